@@ -1,0 +1,226 @@
+"""ctypes wrapper around ``oracle/ubqp_oracle.c`` plus the O8 round loop.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Every function cites the
+passage of PAPER.md (P:n) / SPEC.md (S:n) it follows and the SURVEY.md §8(c)
+definition (O1..O10) restated in DESIGN.md §3.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_SRC = _HERE / "ubqp_oracle.c"
+_LIB = _HERE / "liboracle_ubqp.so"
+_lib = None
+
+__all__ = [
+    "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
+    "glover_params", "diversify", "max_key", "stats", "threshold", "screen", "ascend",
+    "first_derivative_start", "run_rounds",
+]
+
+
+def build_oracle(force: bool = False) -> Path:
+    """Compile the oracle with plain -O2 (no intrinsics, no fast-math, no FMA contraction)."""
+    if force or not _LIB.exists() or _LIB.stat().st_mtime < _SRC.stat().st_mtime:
+        tmp = _LIB.with_suffix(f".so.tmp{os.getpid()}")
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fPIC", "-shared",
+                               "-pthread", str(_SRC), "-o", str(tmp), "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    if _lib is None:
+        build_oracle()
+        lib = ctypes.CDLL(str(_LIB))
+        P = ctypes.c_void_p
+        i64, i32, u64, dbl = ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_double
+        lib.oracle_eval_batch.argtypes = [i32, P, i64, P, P, i32]
+        lib.oracle_eval.argtypes = [i32, P, P]
+        lib.oracle_eval.restype = i64
+        lib.oracle_gains.argtypes = [i32, P, P, P]
+        lib.oracle_splitmix_word.argtypes = [u64, i64, i64, i64]
+        lib.oracle_splitmix_word.restype = u64
+        lib.oracle_random.argtypes = [i32, u64, i64, i32, i32, P]
+        lib.oracle_glover_params.argtypes = [i64, i32, P, P, P]
+        lib.oracle_diversify.argtypes = [i32, P, i64, i64, i32, i32, P]
+        lib.oracle_max_key.argtypes = [i64, i64]
+        lib.oracle_max_key.restype = i64
+        lib.oracle_stats.argtypes = [i64, P, i32, i32, P]
+        lib.oracle_threshold.argtypes = [dbl, i64, i64, i64]
+        lib.oracle_threshold.restype = dbl
+        lib.oracle_screen.argtypes = [i64, P, dbl, P]
+        lib.oracle_screen.restype = i64
+        lib.oracle_ascend_batch.argtypes = [i32, P, i64, P, P, P, i32, i32]
+        lib.oracle_first_derivative_start.argtypes = [i32, P, P]
+        _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _Q(Q) -> np.ndarray:
+    Q = np.ascontiguousarray(Q, dtype=np.int32)
+    assert Q.ndim == 2 and Q.shape[0] == Q.shape[1]
+    return Q
+
+
+def _X(X, n) -> np.ndarray:
+    X = np.ascontiguousarray(X, dtype=np.uint8)
+    if X.ndim == 1:
+        X = X.reshape(1, -1)
+    assert X.shape[1] == n
+    return X
+
+
+# O1 -- f(x) = x^t Q x (P:24 eq. (P))
+def xQx(Q, x) -> int:
+    Q = _Q(Q)
+    x = _X(x, Q.shape[0])
+    return int(_L().oracle_eval(Q.shape[0], _p(Q), _p(x)))
+
+
+def eval_batch(Q, X, nthreads: int = 1) -> np.ndarray:
+    """O1 over a batch ("evaluate ... 1000 samples")."""
+    Q = _Q(Q)
+    n = Q.shape[0]
+    X = _X(X, n)
+    f = np.zeros(X.shape[0], dtype=np.int64)
+    _L().oracle_eval_batch(n, _p(Q), X.shape[0], _p(X), _p(f), int(nthreads))
+    return f
+
+
+# O2 -- Delta_i = (1-2x_i)(Q_ii + 2 sum_{j!=i} Q_ij x_j)
+def gains(Q, x) -> np.ndarray:
+    Q = _Q(Q)
+    n = Q.shape[0]
+    x = _X(x, n)
+    d = np.zeros(n, dtype=np.int64)
+    _L().oracle_gains(n, _p(Q), _p(x), _p(d))
+    return d
+
+
+# O3 -- random solutions from SplitMix64 (R12)
+def splitmix_word(seed: int, g: int, W64: int, w: int) -> int:
+    return int(_L().oracle_splitmix_word(seed & (2**64 - 1), g, W64, w))
+
+
+def random_solutions(n: int, seed: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+    X = np.zeros((k_local, n), dtype=np.uint8)
+    _L().oracle_random(n, seed & (2**64 - 1), k_local, rank, world, _p(X))
+    return X
+
+
+# O4 -- Glover diversification generator (R11)
+def glover_params(t: int, n: int):
+    h, q, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int()
+    _L().oracle_glover_params(t, n, ctypes.byref(h), ctypes.byref(q), ctypes.byref(c))
+    return h.value, q.value, c.value
+
+
+def diversify(seed_x, t0: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+    seed_x = np.ascontiguousarray(seed_x, dtype=np.uint8).reshape(-1)
+    n = seed_x.shape[0]
+    X = np.zeros((k_local, n), dtype=np.uint8)
+    _L().oracle_diversify(n, _p(seed_x), t0, k_local, rank, world, _p(X))
+    return X
+
+
+# O5 -- stats {sum, count, max_key} (R14)
+def max_key(f: int, g: int) -> int:
+    return int(_L().oracle_max_key(f, g))
+
+
+def stats(f, rank: int = 0, world: int = 1) -> np.ndarray:
+    f = np.ascontiguousarray(f, dtype=np.int64)
+    out = np.zeros(4, dtype=np.int64)
+    _L().oracle_stats(f.shape[0], _p(f), rank, world, _p(out))
+    return out
+
+
+# O6 -- T(lambda) = Mean + lambda (Max - Mean); survivors f > T ascending
+def threshold(lam: float, mean_sum: int, mean_count: int, max_value: int) -> float:
+    return float(_L().oracle_threshold(float(lam), int(mean_sum), int(mean_count), int(max_value)))
+
+
+def screen(f, T: float) -> np.ndarray:
+    f = np.ascontiguousarray(f, dtype=np.int64)
+    s = np.zeros(max(1, f.shape[0]), dtype=np.int32)
+    m = _L().oracle_screen(f.shape[0], _p(f), float(T), _p(s))
+    return s[:m].copy()
+
+
+# O7 -- steepest ascent (R9)
+def ascend(Q, X, f, max_flips: int, nthreads: int = 1):
+    """Returns (X_final uint8 [m][n], f_final int64 [m], flips int32 [m]); inputs untouched."""
+    Q = _Q(Q)
+    n = Q.shape[0]
+    X = _X(X, n).copy()
+    f = np.ascontiguousarray(f, dtype=np.int64).copy()
+    flips = np.zeros(X.shape[0], dtype=np.int32)
+    _L().oracle_ascend_batch(n, _p(Q), X.shape[0], _p(X), _p(f), _p(flips), int(max_flips),
+                             int(nthreads))
+    return X, f, flips
+
+
+# first-derivative start
+def first_derivative_start(Q) -> np.ndarray:
+    Q = _Q(Q)
+    x = np.zeros(Q.shape[0], dtype=np.uint8)
+    _L().oracle_first_derivative_start(Q.shape[0], _p(Q), _p(x))
+    return x
+
+
+# O8 -- batched rounds of Figure 2 (R5, R6, R13)
+def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
+               world: int = 1, nthreads: int = 1):
+    """Round 0: K random starts (O3, seed ``sample_seed``) -> pinned (mean_sum, mean_count)
+    ("the mean is the average xQx value derived during sampling").  Incumbent =
+    first-derivative start.  Round r >= 1: diversify from the incumbent with
+    t0 = (r-1)*K ("Diversify(x, best_xQx, i, ...)"), evaluate, Max = max(incumbent,
+    batch max) (R6), screen, ascend survivors, replace the incumbent iff the
+    best ascended f is strictly greater, ties -> lowest g (R8, R14).
+    ``world`` shards every batch cyclically (O10); results must not depend on it.
+    Returns (best_value, best_x, trajectory[list of (round, best_value)])."""
+    Q = _Q(Q)
+    n = Q.shape[0]
+
+    def shards(make):
+        return [make(r) for r in range(world)]
+
+    f0 = [eval_batch(Q, Xr, nthreads) for Xr in shards(
+        lambda r: random_solutions(n, sample_seed, len(range(r, K, world)), r, world))]
+    mean_sum = int(sum(int(fr.sum()) for fr in f0))
+    mean_count = K
+    inc_x = first_derivative_start(Q)
+    inc_f = xQx(Q, inc_x)
+    traj = [(0, inc_f)]
+    for rnd in range(1, rounds + 1):
+        t0 = (rnd - 1) * K
+        best_key, best = -1, None
+        Xs = shards(lambda r: diversify(inc_x, t0, len(range(r, K, world)), r, world))
+        fs = [eval_batch(Q, Xr, nthreads) for Xr in Xs]
+        batch_max = max(int(fr.max()) for fr in fs if fr.size)
+        T = threshold(lam, mean_sum, mean_count, max(inc_f, batch_max))
+        for r in range(world):
+            s = screen(fs[r], T)
+            if s.size == 0:
+                continue
+            Xa, fa, _ = ascend(Q, Xs[r][s], fs[r][s], max_flips, nthreads)
+            for i, slot in enumerate(s):
+                key = max_key(int(fa[i]), r + int(slot) * world)
+                if key > best_key:
+                    best_key, best = key, (int(fa[i]), Xa[i].copy())
+        if best is not None and best[0] > inc_f:
+            inc_f, inc_x = best
+            traj.append((rnd, inc_f))
+    return inc_f, inc_x, traj

@@ -1,0 +1,350 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (not against itself).
+
+Every oracle function (O1..O8) is checked here against an independent fact:
+SPEC worked examples (tests/golden/spec_examples.json), closed forms, brute-force
+enumeration on tiny inputs, library routines (numpy matmul), identities of symmetric
+quadratic forms, the SplitMix64 known answers and Glover's own illustration.
+"""
+import itertools
+import json
+import math
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import generate_Q, pack_bits, unpack_bits
+
+GOLD = Path(__file__).resolve().parent / "golden"
+SPEC = json.loads((GOLD / "spec_examples.json").read_text())
+
+
+def _Qn(name):
+    return np.array(SPEC[name], dtype=np.int32)
+
+
+def _all_x(n):
+    return np.array(list(itertools.product([0, 1], repeat=n)), dtype=np.uint8)[:, ::-1].copy()
+
+
+# ---------------------------------------------------------------- O1 eval
+def test_spec_eval_examples():
+    for e in SPEC["eval"]:
+        assert oracle.xQx(_Qn(e["Q"]), e["x"]) == e["f"], e["cite"]
+    for e in SPEC["eval_batch"]:
+        assert oracle.eval_batch(_Qn(e["Q"]), e["X"]).tolist() == e["f"], e["cite"]
+
+
+def test_eval_closed_forms():
+    rng = np.random.default_rng(11)
+    for n in (1, 2, 7, 33, 64, 65, 130):
+        Q = generate_Q(n, 0.7, -100, 100, seed=int(rng.integers(1 << 30)))
+        zero = np.zeros(n, np.uint8)
+        ones = np.ones(n, np.uint8)
+        assert oracle.xQx(Q, zero) == 0                              # f(0) = 0
+        assert oracle.xQx(Q, ones) == int(Q.astype(np.int64).sum())  # f(1) = sum Q
+        E = np.eye(n, dtype=np.uint8)
+        assert oracle.eval_batch(Q, E).tolist() == np.diag(Q).astype(np.int64).tolist()  # f(e_i)=Q_ii
+
+
+def test_eval_matches_library_matmul_and_complement_identity():
+    rng = np.random.default_rng(12)
+    for n in (3, 50, 129):
+        Q = generate_Q(n, 0.5, -100, 100, seed=int(rng.integers(1 << 30)))
+        X = rng.integers(0, 2, size=(40, n)).astype(np.uint8)
+        f = oracle.eval_batch(Q, X, nthreads=3)
+        Q64 = Q.astype(np.int64)
+        ref = np.einsum("ki,ij,kj->k", X.astype(np.int64), Q64, X.astype(np.int64))
+        assert f.tolist() == ref.tolist()
+        # complement: f(1-x) = sum Q - 2 rowsum^T x + f(x)  (symmetric Q)
+        fc = oracle.eval_batch(Q, 1 - X)
+        rs = Q64.sum(axis=1)
+        assert fc.tolist() == (Q64.sum() - 2 * X.astype(np.int64) @ rs + f).tolist()
+
+
+def test_eval_brute_force_global_optimum_spec():
+    Q3 = _Qn("Q3")
+    X = _all_x(3)
+    f = oracle.eval_batch(Q3, X)
+    assert f.max() == 4 and X[f.argmax()].tolist() == [1, 0, 1]    # S:133 global max
+    # exhaustive average == closed-form expectation
+    assert Fraction(int(f.sum()), len(f)) == Fraction(-1, 2)
+
+
+def test_eval_thread_count_invariance():
+    Q = generate_Q(100, 0.5, -10, 10, seed=5)
+    X = np.random.default_rng(5).integers(0, 2, size=(1000, 100)).astype(np.uint8)
+    a = oracle.eval_batch(Q, X, 1)
+    for t in (2, 8):
+        assert np.array_equal(a, oracle.eval_batch(Q, X, t))
+
+
+# ---------------------------------------------------------------- O2 gains
+def test_spec_gain_examples():
+    for e in SPEC["gains"]:
+        assert oracle.gains(_Qn(e["Q"]), e["x"]).tolist() == e["Delta"], e["cite"]
+
+
+def test_gains_equal_brute_force_flip_differences():
+    rng = np.random.default_rng(13)
+    for n in (1, 2, 5, 17, 64):
+        Q = generate_Q(n, 0.6, -100, 100, seed=int(rng.integers(1 << 30)))
+        for _ in range(5):
+            x = rng.integers(0, 2, size=n).astype(np.uint8)
+            f = oracle.xQx(Q, x)
+            flipped = np.tile(x, (n, 1)) ^ np.eye(n, dtype=np.uint8)
+            brute = oracle.eval_batch(Q, flipped) - f                 # f(x xor e_i) - f(x)
+            assert oracle.gains(Q, x).tolist() == brute.tolist()
+            # Appendix-A identity with Y = Qx from numpy: Delta = Q_ii + 2(1-2x)Y
+            Y = Q.astype(np.int64) @ x.astype(np.int64)
+            assert oracle.gains(Q, x).tolist() == (np.diag(Q) + 2 * (1 - 2 * x.astype(np.int64)) * Y).tolist()
+
+
+# ---------------------------------------------------------------- O3 random bits
+def test_splitmix64_known_answers():
+    for line in (GOLD / "splitmix64_kat.txt").read_text().splitlines():
+        if line.startswith("#") or not line.strip():
+            continue
+        w, v = line.split()
+        assert oracle.splitmix_word(0, 0, 3, int(w)) == int(v, 16)
+
+
+def test_random_solution_bits_layout_and_balance():
+    n = 130
+    X = oracle.random_solutions(n, 77, 64)
+    W = (n + 63) // 64
+    for g in (0, 5, 63):
+        for j in (0, 63, 64, 129):
+            assert X[g, j] == (oracle.splitmix_word(77, g, W, j // 64) >> (j % 64)) & 1
+    big = oracle.random_solutions(257, 3, 2000)
+    p = big.mean()
+    assert abs(p - 0.5) < 4 * math.sqrt(0.25 / big.size)
+
+
+def test_random_sharding_is_cyclic():
+    n, K = 70, 23
+    full = oracle.random_solutions(n, 9, K)
+    for world in (2, 3, 4):
+        for r in range(world):
+            part = oracle.random_solutions(n, 9, len(range(r, K, world)), r, world)
+            assert np.array_equal(part, full[r::world])
+
+
+def test_sampled_mean_matches_expectation():
+    """E f = sum_i Q_ii/2 + sum_{i!=j} Q_ij/4 under iid Bernoulli(1/2) bits."""
+    hits = 0
+    for s in range(20):
+        Q = generate_Q(50, 0.5, -10, 10, seed=1000 + s)
+        f = oracle.eval_batch(Q, oracle.random_solutions(50, s, 10000), nthreads=4)
+        Q64 = Q.astype(np.int64)
+        E = np.trace(Q64) / 2 + (Q64.sum() - np.trace(Q64)) / 4
+        se = f.std(ddof=1) / math.sqrt(f.size)
+        hits += abs(f.mean() - E) <= 3 * se
+    assert hits >= 18
+
+
+# ---------------------------------------------------------------- O4 Glover diversification
+def test_glover_illustration_from_zero_seed():
+    n = 10
+    for line in (GOLD / "glover_n10.txt").read_text().splitlines():
+        if line.startswith("#") or not line.strip():
+            continue
+        h, q, c, bits = line.split()
+        h, q, c = int(h), int(q), int(c)
+        t = h * (h - 1) + 2 * (q - 1) + c              # position of (h,q,c) in the enumeration
+        assert oracle.glover_params(t, n) == (h, q, c)
+        x = oracle.diversify(np.zeros(n, np.uint8), t, 1)[0]
+        assert "".join(map(str, x.tolist())) == bits
+
+
+def test_glover_index_map_enumerates_all_triples_in_order():
+    n = 39
+    expect = [(h, q, c) for h in range(1, n + 1) for q in range(1, h + 1) for c in (0, 1)]
+    assert len(expect) == n * (n + 1)
+    got = [oracle.glover_params(t, n) for t in range(n * (n + 1))]
+    assert got == expect
+    assert oracle.glover_params(n * (n + 1) + 5, n) == expect[5]   # wraps mod n(n+1)
+
+
+def test_glover_hamming_distances_and_duplicates():
+    rng = np.random.default_rng(14)
+    n = 97
+    seed = rng.integers(0, 2, size=n).astype(np.uint8)
+    K = 600
+    X = oracle.diversify(seed, 0, K)
+    for t in range(K):
+        h, q, c = oracle.glover_params(t, n)
+        size = (n - q) // h + 1                       # |M(h,q)| = floor((n-q)/h) + 1
+        dist = int((X[t] != seed).sum())
+        assert dist == (size if c == 0 else n - size)
+    assert np.array_equal(X[1], seed)                # t = 1 (h=1, q=1, c=1) is the seed itself
+    assert np.array_equal(X[4], X[3]) and np.array_equal(X[5], X[2])  # (2,2,c) == (2,1,1-c)
+
+
+def test_glover_sharding_is_cyclic():
+    n, K = 40, 31
+    seed = np.random.default_rng(1).integers(0, 2, size=n).astype(np.uint8)
+    full = oracle.diversify(seed, 17, K)
+    for world in (2, 5):
+        for r in range(world):
+            assert np.array_equal(oracle.diversify(seed, 17, len(range(r, K, world)), r, world),
+                                  full[r::world])
+
+
+# ---------------------------------------------------------------- O5 stats
+def test_stats_sum_count_and_key_order():
+    rng = np.random.default_rng(15)
+    f = rng.integers(-10**9, 10**9, size=300)
+    f[[3, 77, 200]] = 10**9 + 5                     # ties on the max -> lowest g wins
+    for world, rank in ((1, 0), (3, 2)):
+        s = oracle.stats(f, rank, world)
+        assert s[0] == int(f.sum()) and s[1] == f.size
+        g = rank + np.arange(f.size) * world
+        best = max(zip(f.tolist(), (-g).tolist()))   # highest f, then lowest g
+        key = s[2]
+        assert (key >> 22) - (1 << 40) == best[0]
+        assert (1 << 22) - 1 - (key & ((1 << 22) - 1)) == -best[1]
+
+
+def test_max_key_is_monotone():
+    assert oracle.max_key(5, 0) > oracle.max_key(4, 0) > oracle.max_key(4, 1)
+    assert oracle.max_key(-(1 << 40) + 1, (1 << 22) - 1) >= 0
+
+
+# ---------------------------------------------------------------- O6 screen
+def test_spec_threshold_examples():
+    for e in SPEC["threshold"]:
+        assert oracle.threshold(e["lambda"], e["mean"], 1, e["max"]) == e["T"], e["cite"]
+
+
+def test_screen_strict_and_ascending():
+    f = np.array([5, 150, 151, 149, 200, 150, -3], dtype=np.int64)
+    T = oracle.threshold(0.5, 100, 1, 200)
+    assert T == 150.0
+    assert oracle.screen(f, T).tolist() == [2, 4]     # f == T fails ("exceeds"; R8)
+    assert oracle.screen(f, oracle.threshold(1.0, 100, 1, 200)).tolist() == []  # lambda=1: T=Max
+
+
+def test_screen_against_exact_rational_threshold():
+    rng = np.random.default_rng(16)
+    for _ in range(200):
+        s, c = int(rng.integers(-10**12, 10**12)), int(rng.integers(1, 10**6))
+        mx = int(rng.integers(-10**9, 10**9))
+        lam = float(rng.random())
+        T = oracle.threshold(lam, s, c, mx)
+        mean = Fraction(s, c)
+        exact = mean + Fraction(lam) * (mx - mean)
+        assert abs(Fraction(T) - exact) <= abs(exact) * Fraction(1, 2**50) + Fraction(1, 2**40)
+
+
+# ---------------------------------------------------------------- O7 ascent
+def test_spec_ascent_examples():
+    for e in SPEC["steepest_ascent"]:
+        Q = _Qn(e["Q"])
+        x0 = np.array([e["start"]], np.uint8)
+        X, f, flips = oracle.ascend(Q, x0, [oracle.xQx(Q, x0)], max_flips=100)
+        assert X[0].tolist() == e["x"] and f[0] == e["f"] and flips[0] == e["flips"], e["cite"]
+    e = SPEC["apply_flip"][0]
+    Q = _Qn(e["Q"])
+    X, f, flips = oracle.ascend(Q, np.array([e["x"]], np.uint8), [oracle.xQx(Q, e["x"])], 1)
+    assert X[0].tolist() == e["x_after"] and f[0] == e["f_after"]
+    assert oracle.gains(Q, X[0]).tolist() == e["Delta_after"], e["cite"]
+
+
+def _brute_ascent(Q, x, max_flips):
+    """Steepest ascent by brute force over all 1-flip neighbours, using only O1 values."""
+    x = x.copy()
+    n = len(x)
+    flips = 0
+    while flips < max_flips:
+        f = oracle.xQx(Q, x)
+        nb = np.tile(x, (n, 1)) ^ np.eye(n, dtype=np.uint8)
+        fn = oracle.eval_batch(Q, nb)
+        k = int(np.argmax(fn))                  # numpy argmax: first (lowest) index on ties
+        if fn[k] - f <= 0:
+            break
+        x[k] ^= 1
+        flips += 1
+    return x, oracle.xQx(Q, x), flips
+
+
+def test_ascent_equals_brute_force_neighbourhood_search():
+    rng = np.random.default_rng(17)
+    for n in (1, 2, 6, 13, 40):
+        Q = generate_Q(n, 0.8, -100, 100, seed=int(rng.integers(1 << 30)))
+        X0 = rng.integers(0, 2, size=(12, n)).astype(np.uint8)
+        f0 = oracle.eval_batch(Q, X0)
+        for mf in (3, 10 * n):
+            X, f, flips = oracle.ascend(Q, X0, f0, mf, nthreads=2)
+            for k in range(len(X0)):
+                bx, bf, bfl = _brute_ascent(Q, X0[k], mf)
+                assert X[k].tolist() == bx.tolist() and f[k] == bf and flips[k] == bfl
+
+
+def test_ascent_local_optimality_and_value_consistency():
+    rng = np.random.default_rng(18)
+    for n in (50, 200):
+        Q = generate_Q(n, 0.5, -100, 100, seed=int(rng.integers(1 << 30)))
+        X0 = rng.integers(0, 2, size=(25, n)).astype(np.uint8)
+        X, f, flips = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0), 10 * n)
+        assert np.array_equal(f, oracle.eval_batch(Q, X))
+        for k in range(len(X)):
+            if flips[k] < 10 * n:
+                assert oracle.gains(Q, X[k]).max() <= 0      # 1-flip local optimum
+
+
+# ---------------------------------------------------------------- first-derivative start
+def test_first_derivative_start_spec():
+    for e in SPEC["first_derivative_start"]:
+        x = oracle.first_derivative_start(_Qn(e["Q"]))
+        assert x.tolist() == e["x"] and oracle.xQx(_Qn(e["Q"]), x) == e["f"], e["cite"]
+
+
+# ---------------------------------------------------------------- O8 rounds, O10 sharding
+def test_rounds_reach_spec_optimum():
+    best, x, traj = oracle.run_rounds(_Qn("Q3"), K=12, rounds=2, lam=0.5, max_flips=30, sample_seed=1)
+    assert best == SPEC["run_optimum"][0]["best"]
+
+
+def test_rounds_recover_exhaustive_optimum_desk_scale():
+    hits = 0
+    for s in range(20):
+        Q = generate_Q(12, 0.5, -10, 10, seed=500 + s)
+        opt = int(oracle.eval_batch(Q, _all_x(12)).max())
+        best, x, traj = oracle.run_rounds(Q, K=156, rounds=2, lam=0.3, max_flips=120, sample_seed=s)
+        assert best == oracle.xQx(Q, x) and best <= opt
+        vals = [v for _, v in traj]
+        assert all(b > a for a, b in zip(vals, vals[1:]))   # strictly increasing
+        hits += best == opt
+    assert hits >= 18
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rounds_independent_of_world_size(world):
+    Q = generate_Q(60, 0.5, -100, 100, seed=99)
+    a = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3, world=1)
+    b = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3, world=world)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+# ---------------------------------------------------------------- input generator + layout
+def test_generator_symmetry_density_determinism():
+    Q = generate_Q(100, 0.1, -100, 100, seed=1)
+    assert np.array_equal(Q, Q.T) and np.array_equal(Q, generate_Q(100, 0.1, -100, 100, seed=1))
+    iu = np.triu_indices(100)
+    frac = (Q[iu] != 0).mean()
+    assert abs(frac - 0.1) < 0.03
+    assert np.all(generate_Q(5, 1.0, 1, 1, seed=3) == 1)
+
+
+def test_pack_unpack_roundtrip():
+    rng = np.random.default_rng(2)
+    for n in (1, 63, 64, 65, 130):
+        X = rng.integers(0, 2, size=(7, n)).astype(np.uint8)
+        B = pack_bits(X)
+        assert B.shape == (7, (n + 63) // 64)
+        assert np.array_equal(unpack_bits(B, n), X)
+        j = n - 1
+        assert ((B[:, j >> 6] >> np.uint64(j & 63)) & np.uint64(1)).astype(np.uint8).tolist() == X[:, j].tolist()
