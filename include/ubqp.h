@@ -1,0 +1,169 @@
+/*
+ * ubqp.h — C-ABI of the B200 (sm_100a) hot path of Lewis's GPU diversified
+ * multi-start for the Unconstrained Binary Quadratic Problem (arXiv 1706.00037):
+ *
+ *     (P)  maximise f(x) = x^t Q x,  x in {0,1}^n,  Q symmetric
+ *
+ * One round of the method (Figure 2) is the call sequence
+ *     ubqp_diversify | ubqp_random | ubqp_set_batch   -> a batch of K_r solutions
+ *     ubqp_eval_batch                                 -> f = xQx (+ 1-flip gains, stats)
+ *     [caller all-reduces the stats across ranks]
+ *     ubqp_screen                                     -> survivors of T(lambda)
+ *     ubqp_ascend                                     -> 1-flip local optima + best key
+ * Implemented by libubqp.so (paper_1706_00037_b200/csrc).  No torch types, no NCCL.
+ * Citations: P:n = PAPER.md line n (section in brackets), S:n = SPEC.md line n.
+ *
+ * Conventions (all calls)
+ *  - Return value: UBQP_OK or an error code; never throws.  On error the outputs are
+ *    unspecified and ubqp_last_error(h) holds a message.  UBQP_E_CUDA is sticky: the
+ *    handle must be destroyed.
+ *  - Memory: every array argument may be a DEVICE pointer (on the handle's device)
+ *    or a HOST pointer (pageable or pinned); the library detects which with
+ *    cudaPointerGetAttributes.  Device arrays are read/written in stream order on the
+ *    handle's stream and the call returns without synchronising; host arrays are
+ *    copied through the stream and the call synchronises before returning.  The
+ *    caller owns every buffer it passes; the handle owns Q, the batch and workspace.
+ *  - Solutions: bit j of a solution is bit (j & 63) of 64-bit word (j >> 6); a
+ *    solution is W64 = ceil(n/64) words, least significant bit first.  Padding bits
+ *    (j >= n) are ignored on input and written as 0.
+ *  - Sharding (multi-GPU): slot i of a rank's batch is global solution
+ *    g = rank + i*world; every output depends on g only, so results are identical for
+ *    any world size.  K (global batch) <= 2^22.
+ *  - max_key = ((f + 2^40) << 22) | (2^22 - 1 - g): int64, larger = better; MAX over
+ *    keys picks the highest f, ties to the lowest g (a valid NCCL int64 MAX operand).
+ *    -1 means "no solution".
+ */
+#ifndef UBQP_H
+#define UBQP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ubqp_ctx *ubqp_t;
+
+enum {
+    UBQP_OK = 0,
+    UBQP_E_INVALID = 1,       /* null/negative/mismatched argument, bad slot, non-finite lambda */
+    UBQP_E_NOT_SYMMETRIC = 2, /* Q != Q^t ("square symmetric matrix") */
+    UBQP_E_RANGE = 3,         /* a coefficient outside [-127, 127] or an overflow bound fails */
+    UBQP_E_STATE = 4,         /* call order: no Q loaded, no batch, mean_count <= 0, ... */
+    UBQP_E_NOMEM = 5,         /* device allocation failed */
+    UBQP_E_CUDA = 6           /* CUDA error (sticky) */
+};
+
+/* ubqp_eval_batch flags */
+enum { UBQP_EMIT_GAINS = 1 };
+
+/* batch statistics of ubqp_eval_batch (T(lambda) inputs): sum of f, count,
+ * best max_key; reserved = 0.  int64 so the caller can all-reduce SUM/SUM/MAX. */
+typedef struct {
+    int64_t sum;
+    int64_t count;
+    int64_t max_key;
+    int64_t reserved;
+} ubqp_stats;
+
+/* ABI version (major*100 + minor). */
+int ubqp_version(void);
+
+/* Create a handle bound to CUDA device `device` and stream `cuda_stream`
+ * (a cudaStream_t; NULL = the handle creates and owns a non-blocking stream).
+ * Errors: E_INVALID (out == NULL, bad device), E_CUDA. */
+int ubqp_create(int device, void *cuda_stream, ubqp_t *out);
+
+/* Destroy a handle and free its device memory (synchronises its stream). */
+int ubqp_destroy(ubqp_t h);
+
+/* Message of the last error on h (static string if h == NULL). Never NULL. */
+const char *ubqp_last_error(ubqp_t h);
+
+/* ReadQ/MoveQtoGPU (Figure 2; "the transfer of Q occurs only once").
+ * Q: n*n int32, row-major, host or device.  Validates symmetry (E_NOT_SYMMETRIC) and
+ * |Q_ij| <= 127 (E_RANGE: the evaluation runs on int8 tensor cores, exact),
+ * then builds the device copies: Q8 int8 [ceil(n/256)*256][n_pad] (n_pad =
+ * ceil(n/128)*128, zero padded) and diag int32.  k_max = workspace capacity in
+ * solutions per batch (1 <= k_max <= 2^22).  n >= 1, n <= 16384.  Replaces any earlier
+ * Q and batch.  Synchronises. */
+int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max);
+
+/* Diversify (Figure 2 line "Diversify(x, best_xQx, i, Q_cols)"; Glover 1998
+ * diversification generator; "number of variables to be changed ... based on the
+ * loop counter").  For slot i, t = t0 + g (g = rank + i*world), taken mod n(n+1):
+ *   h = floor((1 + isqrt(1 + 4t))/2), r = t - h(h-1), q = floor(r/2) + 1, c = r mod 2,
+ *   x = seed xor {bits q-1, q-1+h, q-1+2h, ... < n}, complemented within n bits if c = 1.
+ * seed_bits: W64 words.  Fills the handle's batch with k_local solutions (0 <= k_local
+ * <= k_max).  Errors: E_INVALID, E_STATE (no Q). */
+int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_local,
+                   int32_t rank, int32_t world);
+
+/* EvaluateRandomStarts' random solutions: bit j of slot i is bit
+ * (j & 63) of SplitMix64-mix(seed + (g*W64 + (j>>6) + 1) * 0x9E3779B97F4A7C15),
+ * g = rank + i*world.  Fills the batch with k_local solutions. */
+int ubqp_random(ubqp_t h, uint64_t seed, int64_t k_local, int32_t rank, int32_t world);
+
+/* Load caller solutions bits[k_local][W64] as the batch (rank/world set their g). */
+int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank,
+                   int32_t world);
+
+/* CalculateFirstDerivativeSolution (Figure 2; "simply sum the i^th row of Q
+ * ... and if that sum is positive, then set x_i = 1"): bits_out[W64] gets x_i = 1 iff
+ * sum_j Q_ij > 0.  Requires a loaded Q; does not touch the batch. */
+int ubqp_first_derivative(ubqp_t h, uint64_t *bits_out);
+
+/* Copy the current batch out: bits_out[k_local][W64]. */
+int ubqp_get_batch(ubqp_t h, uint64_t *bits_out);
+
+/* Evaluate (Figure 2 "xQx <- Evaluate(x)"; "the GPU, which excels at matrix
+ * multiplication"): for every slot k of the batch, f_k = x_k^t Q x_k computed as
+ * Y = X Q on int8 tensor cores (int32 exact) with the row-dot f_k = sum_j x_kj Y_kj
+ * fused into the epilogue.  flags & UBQP_EMIT_GAINS additionally stores the 1-flip
+ * gains Delta_kj = Q_jj + 2(1 - 2 x_kj) Y_kj = f(x xor e_j) - f(x) on the device
+ * for ubqp_ascend / ubqp_get_gains.  f_out: int64[k_local] (may be NULL); stats_out:
+ * one ubqp_stats (may be NULL) = {sum f, k_local, max_key over the batch, 0}.
+ * Errors: E_STATE (no batch). */
+int ubqp_eval_batch(ubqp_t h, int flags, int64_t *f_out, ubqp_stats *stats_out);
+
+/* Copy gains of slots [slot0, slot0+count) out as int32 [count][n] (requires the last
+ * ubqp_eval_batch to have used UBQP_EMIT_GAINS; else E_STATE). */
+int ubqp_get_gains(ubqp_t h, int64_t slot0, int64_t count, int32_t *gains_out);
+
+/* Screen (Figure 2 "if xQx > Screening_value"; T(lambda) = Mean + lambda(Max - Mean),
+ * P:49): mean = (double)mean_sum/(double)mean_count; T = mean + lambda*(max_value -
+ * mean) in IEEE binary64 without contraction; survivors = {k : f_k > T} = {k : f_k >
+ * floor(T)} of the last evaluated batch, in ascending slot order, written to
+ * surv_out[0..m) (capacity k_local).  *m_out (host) = m; *T_out (host, may be NULL) = T.
+ * Synchronises (m is returned to the host).  Errors: E_INVALID (lambda not finite),
+ * E_STATE (mean_count <= 0 or no evaluated batch). */
+int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count,
+                int64_t max_value, int32_t *surv_out, int64_t *m_out, double *T_out);
+
+/* PerformSteepestAscent ("terminating when no improvements are possible or a
+ * maximum number of flips have been made. No checks for cycling nor tabu lists",
+ * P:93-95; 1-flip method of Glover et al. 2002).  For i < m, starting from batch
+ * slot s = slots[i] (its f and gains from the last ubqp_eval_batch; gains are computed
+ * here if that call did not emit them): repeat  k* = argmax_j Delta_j (lowest j on
+ * ties); stop if Delta_k* <= 0 or flips == max_flips; f += Delta_k*; flip x_k*; update
+ * Delta.  Outputs per i: f_out int64[m], flips_out int32[m], bits_out uint64[m][W64]
+ * (any may be NULL), best_key_out: one int64 = max over i of max_key(f_i, g(s_i))
+ * (-1 if m == 0; may be NULL).  The batch itself is not modified.
+ * Errors: E_INVALID (slot out of range, m > k_local, max_flips < 0), E_STATE. */
+int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
+                int64_t *f_out, int32_t *flips_out, uint64_t *bits_out,
+                int64_t *best_key_out);
+
+/* Wait for all work queued on the handle's stream. */
+int ubqp_sync(ubqp_t h);
+
+/* Introspection (read-only): n, n_pad, W64, k_max, k_local, kernels launched so far. */
+enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
+       UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6 };
+int ubqp_query(ubqp_t h, int what, int64_t *value);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UBQP_H */

@@ -1,0 +1,520 @@
+// abi.cu — the C-ABI of include/ubqp.h: handle, Q residency, workspace, pointer-kind
+// detection, launch order and error mapping.  All arithmetic of the method runs in the
+// kernels of gen.cu / eval_tc.cu / screen.cu / ascend.cu; the host only forms T(lambda)
+// in binary64 and marshals arguments.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "ubqp_internal.cuh"
+
+using ubqp::Ctx;
+
+struct ubqp_ctx : public Ctx {};
+
+namespace {
+
+const char *kNullHandleMsg = "ubqp: null handle";
+
+int fail(ubqp_t h, int code, const char *msg) {
+    if (h) h->err = msg;
+    return code;
+}
+
+int fail_cuda(ubqp_t h, cudaError_t e, const char *where) {
+    if (h) {
+        h->sticky_cuda = true;
+        h->err = std::string("ubqp: CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    }
+    return UBQP_E_CUDA;
+}
+
+#define CK(expr)                                                       \
+    do {                                                               \
+        cudaError_t e_ = (expr);                                       \
+        if (e_ != cudaSuccess) return fail_cuda(h, e_, #expr);         \
+    } while (0)
+
+#define CK_LAUNCH(where)                                               \
+    do {                                                               \
+        cudaError_t e_ = cudaGetLastError();                           \
+        if (e_ != cudaSuccess) return fail_cuda(h, e_, where);         \
+    } while (0)
+
+#define GUARD(h)                                                       \
+    do {                                                               \
+        if (!(h)) return UBQP_E_INVALID;                               \
+        if ((h)->sticky_cuda) return UBQP_E_CUDA;                      \
+        cudaError_t e_ = cudaSetDevice((h)->device);                   \
+        if (e_ != cudaSuccess) return fail_cuda(h, e_, "cudaSetDevice"); \
+    } while (0)
+
+bool is_device_ptr(const void *p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+template <typename T>
+void dfree(T *&p) {
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+void free_batch(Ctx &c) {
+    dfree(c.Xb); dfree(c.X8); dfree(c.f); dfree(c.gains); dfree(c.surv); dfree(c.blk_count);
+    dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots);
+    c.asc_cap = 0;
+    c.k_max = 0; c.k_cap_pad = 0; c.k_local = -1;
+    c.f_valid = c.gains_valid = false;
+}
+
+void free_all(Ctx &c) {
+    free_batch(c);
+    dfree(c.Q8); dfree(c.diag); dfree(c.seed); dfree(c.scratch64);
+    c.n = 0;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                             &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D int8 tensor map: inner dim `cols` bytes (contiguous), outer `rows`, box 128 x box_rows,
+// 128-byte swizzle (the UMMA K-major SW128 canonical layout).
+bool encode_map(CUtensorMap *m, void *base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols};
+    cuuint32_t box[2] = {128u, box_rows};
+    cuuint32_t estr[2] = {1u, 1u};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int ensure_gains(ubqp_t h) {
+    if (h->gains) return UBQP_OK;
+    size_t bytes = static_cast<size_t>(h->k_max) * h->n_pad * sizeof(int32_t);
+    cudaError_t e = cudaMalloc(&h->gains, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        h->gains = nullptr;
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the gains buffer");
+    }
+    return UBQP_OK;
+}
+
+int ensure_asc(ubqp_t h, int64_t m) {
+    if (m <= h->asc_cap) return UBQP_OK;
+    dfree(h->asc_f); dfree(h->asc_flips); dfree(h->asc_bits); dfree(h->asc_slots);
+    int64_t cap = m;
+    if (cudaMalloc(&h->asc_f, cap * sizeof(int64_t)) != cudaSuccess ||
+        cudaMalloc(&h->asc_flips, cap * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->asc_bits, cap * h->W64 * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMalloc(&h->asc_slots, cap * sizeof(int32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        h->asc_cap = 0;
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate ascent buffers");
+    }
+    h->asc_cap = cap;
+    return UBQP_OK;
+}
+
+// run the evaluation GEMM (+ stats into scratch64[0..3]) on the current batch
+int run_eval(ubqp_t h, bool emit_gains) {
+    if (emit_gains) {
+        int rc = ensure_gains(h);
+        if (rc) return rc;
+    }
+    const int64_t k = h->k_local;
+    if (k > 0) CK(cudaMemsetAsync(h->f, 0, k * sizeof(int64_t), h->stream));
+    ubqp::launch_eval_tc(*h, k, emit_gains);
+    CK_LAUNCH("eval_tc_kernel");
+    ubqp::launch_stats(*h, k, h->scratch64);
+    CK_LAUNCH("stats_kernel");
+    h->f_valid = true;
+    h->gains_valid = emit_gains;
+    return UBQP_OK;
+}
+
+int check_batch_args(ubqp_t h, int64_t k_local, int32_t rank, int32_t world) {
+    if (h->n <= 0) return fail(h, UBQP_E_STATE, "ubqp: no Q loaded");
+    if (k_local < 0 || k_local > h->k_max) return fail(h, UBQP_E_INVALID, "ubqp: k_local out of [0, k_max]");
+    if (world < 1 || rank < 0 || rank >= world) return fail(h, UBQP_E_INVALID, "ubqp: bad rank/world");
+    if (k_local > 0 && static_cast<int64_t>(rank) + (k_local - 1) * world >= (1ll << 22))
+        return fail(h, UBQP_E_INVALID, "ubqp: global index g exceeds 2^22");
+    return UBQP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ubqp_version(void) { return 100; }
+
+int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
+    if (!out) return UBQP_E_INVALID;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || device < 0 || device >= count) {
+        cudaGetLastError();
+        return UBQP_E_INVALID;
+    }
+    ubqp_t h = new (std::nothrow) ubqp_ctx();
+    if (!h) return UBQP_E_NOMEM;
+    h->device = device;
+    if (cudaSetDevice(device) != cudaSuccess) { delete h; return UBQP_E_CUDA; }
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (major != 10 || minor != 0) {
+        delete h;
+        return UBQP_E_INVALID;   // built for sm_100a (B200) only
+    }
+    if (cuda_stream) {
+        h->stream = static_cast<cudaStream_t>(cuda_stream);
+    } else {
+        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete h;
+            return UBQP_E_CUDA;
+        }
+        h->own_stream = true;
+    }
+    if (cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)) != cudaSuccess) {
+        if (h->own_stream) cudaStreamDestroy(h->stream);
+        delete h;
+        return UBQP_E_NOMEM;
+    }
+    *out = h;
+    return UBQP_OK;
+}
+
+int ubqp_destroy(ubqp_t h) {
+    if (!h) return UBQP_E_INVALID;
+    cudaSetDevice(h->device);
+    cudaStreamSynchronize(h->stream);
+    free_all(*h);
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return UBQP_OK;
+}
+
+const char *ubqp_last_error(ubqp_t h) {
+    if (!h) return kNullHandleMsg;
+    return h->err.c_str();
+}
+
+int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
+    GUARD(h);
+    if (!Q || n < 1 || n > 16384) return fail(h, UBQP_E_INVALID, "ubqp: n must be in [1, 16384]");
+    if (k_max < 1 || k_max > (1ll << 22)) return fail(h, UBQP_E_INVALID, "ubqp: k_max must be in [1, 2^22]");
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    std::vector<int32_t> hq;
+    const int32_t *Qh = Q;
+    if (is_device_ptr(Q)) {
+        hq.resize(nn);
+        CK(cudaMemcpy(hq.data(), Q, nn * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        Qh = hq.data();
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const int32_t v = Qh[static_cast<int64_t>(i) * n + j];
+            if (v < -127 || v > 127) return fail(h, UBQP_E_RANGE, "ubqp: |Q_ij| > 127 (int8 tensor-core path)");
+            if (j > i && v != Qh[static_cast<int64_t>(j) * n + i])
+                return fail(h, UBQP_E_NOT_SYMMETRIC, "ubqp: Q is not symmetric");
+        }
+    CK(cudaStreamSynchronize(h->stream));
+    free_all(*h);
+    CK(cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)));
+    h->n = n;
+    h->n_pad = (n + ubqp::kNPadAlign - 1) / ubqp::kNPadAlign * ubqp::kNPadAlign;
+    h->q_rows = (n + ubqp::kQRowAlign - 1) / ubqp::kQRowAlign * ubqp::kQRowAlign;
+    h->W64 = (n + 63) / 64;
+    std::vector<int8_t> q8(static_cast<size_t>(h->q_rows) * h->n_pad, 0);
+    std::vector<int32_t> dg(h->q_rows, 0);
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j)
+            q8[static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
+        dg[i] = Qh[static_cast<int64_t>(i) * n + i];
+    }
+    if (cudaMalloc(&h->Q8, q8.size()) != cudaSuccess || cudaMalloc(&h->diag, dg.size() * 4) != cudaSuccess ||
+        cudaMalloc(&h->seed, h->W64 * sizeof(uint64_t)) != cudaSuccess) {
+        cudaGetLastError();
+        free_all(*h);
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate Q");
+    }
+    CK(cudaMemcpy(h->Q8, q8.data(), q8.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->diag, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
+    // batch workspace
+    h->k_max = k_max;
+    h->k_cap_pad = (k_max + ubqp::kBM - 1) / ubqp::kBM * ubqp::kBM;
+    const int64_t nblk = (k_max + 4095) / 4096 + 1;
+    if (cudaMalloc(&h->Xb, k_max * h->W64 * sizeof(uint64_t)) != cudaSuccess ||
+        cudaMalloc(&h->X8, h->k_cap_pad * h->n_pad) != cudaSuccess ||
+        cudaMalloc(&h->f, k_max * sizeof(int64_t)) != cudaSuccess ||
+        cudaMalloc(&h->surv, k_max * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->blk_count, nblk * sizeof(int32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        free_all(*h);
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the batch workspace");
+    }
+    CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
+    if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM) ||
+        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN)) {
+        free_all(*h);
+        return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
+    }
+    h->k_local = -1;
+    CK(cudaDeviceSynchronize());
+    return UBQP_OK;
+}
+
+int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_local, int32_t rank,
+                   int32_t world) {
+    GUARD(h);
+    int rc = check_batch_args(h, k_local, rank, world);
+    if (rc) return rc;
+    if (!seed_bits) return fail(h, UBQP_E_INVALID, "ubqp: seed_bits is NULL");
+    if (t0 < 0) return fail(h, UBQP_E_INVALID, "ubqp: t0 < 0");
+    const uint64_t *seed_dev = seed_bits;
+    if (!is_device_ptr(seed_bits)) {
+        CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+        seed_dev = h->seed;
+    }
+    h->rank = rank;
+    h->world = world;
+    h->k_local = k_local;
+    h->f_valid = h->gains_valid = false;
+    ubqp::launch_glover(*h, seed_dev, t0, k_local);
+    CK_LAUNCH("glover_kernel");
+    return UBQP_OK;
+}
+
+int ubqp_random(ubqp_t h, uint64_t seed, int64_t k_local, int32_t rank, int32_t world) {
+    GUARD(h);
+    int rc = check_batch_args(h, k_local, rank, world);
+    if (rc) return rc;
+    h->rank = rank;
+    h->world = world;
+    h->k_local = k_local;
+    h->f_valid = h->gains_valid = false;
+    ubqp::launch_random(*h, seed, k_local);
+    CK_LAUNCH("random_kernel");
+    return UBQP_OK;
+}
+
+int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank, int32_t world) {
+    GUARD(h);
+    int rc = check_batch_args(h, k_local, rank, world);
+    if (rc) return rc;
+    if (!bits && k_local > 0) return fail(h, UBQP_E_INVALID, "ubqp: bits is NULL");
+    const size_t bytes = static_cast<size_t>(k_local) * h->W64 * sizeof(uint64_t);
+    if (bytes) {
+        CK(cudaMemcpyAsync(h->Xb, bits, bytes, is_device_ptr(bits) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           h->stream));
+    }
+    h->rank = rank;
+    h->world = world;
+    h->k_local = k_local;
+    h->f_valid = h->gains_valid = false;
+    ubqp::launch_expand(*h, k_local);
+    CK_LAUNCH("expand_kernel");
+    return UBQP_OK;
+}
+
+int ubqp_first_derivative(ubqp_t h, uint64_t *bits_out) {
+    GUARD(h);
+    if (h->n <= 0) return fail(h, UBQP_E_STATE, "ubqp: no Q loaded");
+    if (!bits_out) return fail(h, UBQP_E_INVALID, "ubqp: bits_out is NULL");
+    const bool dev = is_device_ptr(bits_out);
+    uint64_t *dst = dev ? bits_out : h->seed;
+    ubqp::launch_first_derivative(*h, dst);
+    CK_LAUNCH("first_derivative_kernel");
+    if (!dev) {
+        CK(cudaMemcpyAsync(bits_out, dst, h->W64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return UBQP_OK;
+}
+
+int ubqp_get_batch(ubqp_t h, uint64_t *bits_out) {
+    GUARD(h);
+    if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch");
+    if (!bits_out) return fail(h, UBQP_E_INVALID, "ubqp: bits_out is NULL");
+    const size_t bytes = static_cast<size_t>(h->k_local) * h->W64 * sizeof(uint64_t);
+    if (!bytes) return UBQP_OK;
+    if (is_device_ptr(bits_out)) {
+        CK(cudaMemcpyAsync(bits_out, h->Xb, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    } else {
+        CK(cudaMemcpyAsync(bits_out, h->Xb, bytes, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    return UBQP_OK;
+}
+
+int ubqp_eval_batch(ubqp_t h, int flags, int64_t *f_out, ubqp_stats *stats_out) {
+    GUARD(h);
+    if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch to evaluate");
+    if (flags & ~UBQP_EMIT_GAINS) return fail(h, UBQP_E_INVALID, "ubqp: unknown flags");
+    int rc = run_eval(h, (flags & UBQP_EMIT_GAINS) != 0);
+    if (rc) return rc;
+    bool sync = false;
+    const int64_t k = h->k_local;
+    if (f_out && k > 0) {
+        const bool dev = is_device_ptr(f_out);
+        CK(cudaMemcpyAsync(f_out, h->f, k * sizeof(int64_t), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           h->stream));
+        sync |= !dev;
+    }
+    if (stats_out) {
+        const bool dev = is_device_ptr(stats_out);
+        CK(cudaMemcpyAsync(stats_out, h->scratch64, sizeof(ubqp_stats),
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+        sync |= !dev;
+    }
+    if (sync) CK(cudaStreamSynchronize(h->stream));
+    return UBQP_OK;
+}
+
+int ubqp_get_gains(ubqp_t h, int64_t slot0, int64_t count, int32_t *gains_out) {
+    GUARD(h);
+    if (!h->gains_valid) return fail(h, UBQP_E_STATE, "ubqp: last eval did not emit gains");
+    if (slot0 < 0 || count < 0 || slot0 + count > h->k_local || (!gains_out && count))
+        return fail(h, UBQP_E_INVALID, "ubqp: bad gains range");
+    if (!count) return UBQP_OK;
+    const bool dev = is_device_ptr(gains_out);
+    CK(cudaMemcpy2DAsync(gains_out, h->n * sizeof(int32_t), h->gains + slot0 * h->n_pad, h->n_pad * sizeof(int32_t),
+                         h->n * sizeof(int32_t), count, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         h->stream));
+    if (!dev) CK(cudaStreamSynchronize(h->stream));
+    return UBQP_OK;
+}
+
+int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count, int64_t max_value,
+                int32_t *surv_out, int64_t *m_out, double *T_out) {
+    GUARD(h);
+    if (!std::isfinite(lambda)) return fail(h, UBQP_E_INVALID, "ubqp: lambda is not finite");
+    if (mean_count <= 0) return fail(h, UBQP_E_STATE, "ubqp: mean_count <= 0");
+    if (!h->f_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated batch");
+    if (!m_out || (!surv_out && h->k_local > 0)) return fail(h, UBQP_E_INVALID, "ubqp: null output");
+    // T(lambda) = Mean + lambda (Max - Mean), binary64, one rounding per operation
+    volatile double mean = static_cast<double>(mean_sum) / static_cast<double>(mean_count);
+    volatile double diff = static_cast<double>(max_value) - mean;
+    volatile double scaled = lambda * diff;
+    const double T = mean + scaled;
+    if (T_out) *T_out = T;
+    // f > T  <=>  f > floor(T) for integer f; clamp to the int64 range
+    int64_t t_floor;
+    const double fl = std::floor(T);
+    if (std::isnan(T)) return fail(h, UBQP_E_INVALID, "ubqp: T is NaN");
+    if (fl >= 9.2233720368547758e18) t_floor = INT64_MAX;
+    else if (fl < -9.2233720368547758e18) t_floor = INT64_MIN;
+    else t_floor = static_cast<int64_t>(fl);
+    const int64_t k = h->k_local;
+    ubqp::launch_screen(*h, k, t_floor, h->scratch64 + 4);
+    CK_LAUNCH("screen kernels");
+    int64_t m = 0;
+    CK(cudaMemcpyAsync(&m, h->scratch64 + 4, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (m > 0) {
+        const bool dev = is_device_ptr(surv_out);
+        if (!dev || surv_out != h->surv) {
+            CK(cudaMemcpyAsync(surv_out, h->surv, m * sizeof(int32_t), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                               h->stream));
+            if (!dev) CK(cudaStreamSynchronize(h->stream));
+        }
+    }
+    *m_out = m;
+    return UBQP_OK;
+}
+
+int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_out,
+                int32_t *flips_out, uint64_t *bits_out, int64_t *best_key_out) {
+    GUARD(h);
+    if (!h->f_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated batch");
+    if (m < 0 || m > h->k_local || max_flips < 0 || (!slots && m > 0))
+        return fail(h, UBQP_E_INVALID, "ubqp: bad ascend arguments");
+    if (!h->gains_valid) {
+        int rc = run_eval(h, true);     // gains of the whole batch (K-GAIN)
+        if (rc) return rc;
+    }
+    int rc = ensure_asc(h, m > 0 ? m : 1);
+    if (rc) return rc;
+    // slots
+    const int32_t *slots_dev = slots;
+    if (m > 0 && !is_device_ptr(slots)) {
+        for (int64_t i = 0; i < m; ++i)
+            if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        slots_dev = h->asc_slots;
+    }
+    const bool f_dev = f_out && is_device_ptr(f_out);
+    const bool fl_dev = flips_out && is_device_ptr(flips_out);
+    const bool b_dev = bits_out && is_device_ptr(bits_out);
+    const bool k_dev = best_key_out && is_device_ptr(best_key_out);
+    int64_t *f_d = f_dev ? f_out : h->asc_f;
+    int32_t *fl_d = fl_dev ? flips_out : h->asc_flips;
+    uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
+    int64_t *k_d = k_dev ? best_key_out : h->scratch64 + 5;
+    CK(cudaMemsetAsync(k_d, 0xFF, sizeof(int64_t), h->stream));     // -1 = none
+    if (ubqp::launch_ascend(*h, slots_dev, m, max_flips, f_d, fl_d, b_d, k_d))
+        return fail(h, UBQP_E_RANGE, "ubqp: n outside the ascent kernel range");
+    CK_LAUNCH("ascend_kernel");
+    bool sync = false;
+    if (f_out && !f_dev && m) { CK(cudaMemcpyAsync(f_out, f_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (flips_out && !fl_dev && m) { CK(cudaMemcpyAsync(flips_out, fl_d, m * 4, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (bits_out && !b_dev && m) {
+        CK(cudaMemcpyAsync(bits_out, b_d, m * h->W64 * 8, cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
+    }
+    if (best_key_out && !k_dev) { CK(cudaMemcpyAsync(best_key_out, k_d, 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (sync) CK(cudaStreamSynchronize(h->stream));
+    if (!fl_dev && flips_out) {
+        for (int64_t i = 0; i < m; ++i)
+            if (flips_out[i] < 0) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+    }
+    return UBQP_OK;
+}
+
+int ubqp_sync(ubqp_t h) {
+    GUARD(h);
+    CK(cudaStreamSynchronize(h->stream));
+    return UBQP_OK;
+}
+
+int ubqp_query(ubqp_t h, int what, int64_t *value) {
+    if (!h || !value) return UBQP_E_INVALID;
+    switch (what) {
+        case UBQP_Q_N: *value = h->n; break;
+        case UBQP_Q_NPAD: *value = h->n_pad; break;
+        case UBQP_Q_W64: *value = h->W64; break;
+        case UBQP_Q_KMAX: *value = h->k_max; break;
+        case UBQP_Q_KLOCAL: *value = h->k_local; break;
+        case UBQP_Q_LAUNCHES: *value = h->launches; break;
+        case UBQP_Q_STREAM: *value = reinterpret_cast<int64_t>(h->stream); break;
+        default: return UBQP_E_INVALID;
+    }
+    return UBQP_OK;
+}
+
+}  // extern "C"

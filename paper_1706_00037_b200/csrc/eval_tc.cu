@@ -1,0 +1,243 @@
+// eval_tc.cu — K-EVAL: batched xQx on 5th-generation tensor cores.
+//
+// Y = X8 · Q8  (s8 x s8 -> s32, exact), never written to HBM: the accumulator tile lives
+// in TMEM and the epilogue folds it immediately into
+//     f_k      = sum_j x_kj Y_kj                         (P:24 eq. (P); Appendix A of SURVEY)
+//     Delta_kj = Q_jj + 2 (1 - 2 x_kj) Y_kj              (P:53 1-flip gains; UBQP_EMIT_GAINS)
+// A = X8 [K x n_pad] K-major; B = Q8 [q_rows x n_pad] row-major, which is the "N x K,
+// K-major" operand because Q = Q^t (row j of Q8 = column j of Q).
+//
+// Persistent warp-specialised kernel, one CTA per SM:
+//   warp 0      : TMA producer (128B-swizzled 128x128 A and 256x128 B boxes, kStages ring)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=32)
+//   warps 2..5  : epilogue (tcgen05.ld 32x32b -> f partial / gains), TMEM double-buffered
+// Tiles are ordered n-fastest so the ~5 X bands in flight are shared through L2 by all
+// N tiles and Q (49 MB at n = 7000) stays L2-resident.
+#include "ubqp_internal.cuh"
+
+namespace ubqp {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr uint32_t kABytes = kBM * kBK;             // 16 KB
+constexpr uint32_t kBBytes = kBN * kBK;             // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
+constexpr uint32_t kTmemCols = 2 * kBN;             // two 128 x 256 s32 accumulators
+constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
+constexpr uint32_t kIdesc = dev::idesc_i8(kBM, kBN);
+
+__global__ void __launch_bounds__(kThreads, 1)
+eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ,
+               int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
+               const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
+               int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains) {
+    using namespace dev;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~static_cast<uintptr_t>(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + kStages * kABytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+    uint64_t *empty = full + kStages;
+    uint64_t *tfull = empty + kStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 128);
+        }
+        fence_mbar_init();
+        tma_prefetch(&tmX);
+        tma_prefetch(&tmQ);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            const uint64_t pol_q = policy_evict_last();
+            const uint64_t pol_x = policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                const int m0 = static_cast<int>(tile / num_n_tiles) * kBM;
+                const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
+                for (int kb = 0; kb < num_k_blocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    mbar_arrive_expect_tx(&full[stage], kStageBytes);
+                    tma_load_2d(sA + stage * kABytes, &tmX, kb * kBK, m0, &full[stage], pol_x);
+                    tma_load_2d(sB + stage * kBBytes, &tmQ, kb * kBK, n0, &full[stage], pol_q);
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (one thread issues for the whole CTA)
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+                for (int kb = 0; kb < num_k_blocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
+                    const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kBBytes));
+#pragma unroll
+                    for (int k = 0; k < kBK / kUmmaK; ++k) {
+                        // +32 bytes along K inside the 128B swizzle atom = +2 in the >>4 field
+                        mma_i8(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdesc,
+                               (kb | k) != 0 ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);   // frees the smem slot when these MMAs retire
+                    if (++stage == kStages) { stage = 0; phase ^= 1u; }
+                }
+                mma_commit(&tfull[acc]);         // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+            }
+        }
+    } else {
+        // ---------------- epilogue: warp w may read TMEM lanes 32*(w%4) .. +31
+        const int quarter = warp & 3;
+        const int row_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int64_t m0 = (tile / num_n_tiles) * kBM;
+            const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
+            const int64_t row = m0 + row_in_tile;
+            const bool row_ok = row < K;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            int32_t partial = 0;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                   static_cast<uint32_t>(acc * kBN);
+#pragma unroll 1
+            for (int c = 0; c < kBN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
+                tmem_wait_ld();
+                const int col0 = n0 + c * 32;
+                uint32_t bits = 0;
+                if (row_ok && (col0 >> 6) < W64)
+                    bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
+                if (emit_gains && row_ok && col0 < n_pad) {
+                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+                    int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const int4 d = __ldg(dg + i4);
+                        int o[4];
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = 4 * i4 + e;
+                            const int y2 = 2 * static_cast<int32_t>(v[i]);
+                            o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
+                        }
+                        gp[i4] = make_int4(o[0], o[1], o[2], o[3]);
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+            if (row_ok)
+                atomicAdd(reinterpret_cast<unsigned long long *>(f + row),
+                          static_cast<unsigned long long>(static_cast<int64_t>(partial)));
+            if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------- batch statistics
+__global__ void __launch_bounds__(1024) stats_kernel(const int64_t *__restrict__ f, int64_t K,
+                                                     int rank, int world,
+                                                     int64_t *__restrict__ out) {
+    __shared__ int64_t s_sum[32], s_key[32];
+    int64_t sum = 0, key = -1;
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+        const int64_t v = f[i];
+        sum += v;
+        const int64_t g = static_cast<int64_t>(rank) + i * world;
+        const int64_t k = static_cast<int64_t>(
+            (static_cast<uint64_t>(v + (1ll << 40)) << 22) |
+            static_cast<uint64_t>((1ll << 22) - 1 - g));
+        key = k > key ? k : key;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const int64_t other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other > key ? other : key;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_sum[threadIdx.x >> 5] = sum;
+        s_key[threadIdx.x >> 5] = key;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t S = 0, M = -1;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            S += s_sum[w];
+            M = s_key[w] > M ? s_key[w] : M;
+        }
+        out[0] = S;
+        out[1] = K;
+        out[2] = M;
+        out[3] = 0;
+    }
+}
+
+bool g_attr_set = false;
+
+}  // namespace
+
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains) {
+    if (k <= 0) return;
+    if (!g_attr_set) {
+        cudaFuncSetAttribute(eval_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemBytes));
+        g_attr_set = true;
+    }
+    const int num_n_tiles = (c.n + kBN - 1) / kBN;
+    const int num_k_blocks = c.n_pad / kBK;
+    const int64_t num_m_tiles = (k + kBM - 1) / kBM;
+    const int64_t num_tiles = num_m_tiles * num_n_tiles;
+    const int grid = static_cast<int>(num_tiles < c.num_sms ? num_tiles : c.num_sms);
+    eval_tc_kernel<<<grid, kThreads, kSmemBytes, c.stream>>>(
+        c.tmap_X8, c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb,
+        c.diag, c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+    ++c.launches;
+}
+
+void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev) {
+    stats_kernel<<<1, 1024, 0, c.stream>>>(c.f, k, c.rank, c.world, stats_dev);
+    ++c.launches;
+}
+
+}  // namespace ubqp

@@ -1,0 +1,172 @@
+// gen.cu — K-GEN: on-device generation of the solution batch.
+//
+// One thread per (slot, 64-bit word) of the padded row: it produces the packed word
+// Xb[slot][w] (w < W64) and its byte expansion X8[slot][64w .. 64w+63] (the int8
+// A operand of the evaluation GEMM, zero beyond n).  HBM-write bound:
+// n/8 + n_pad bytes per solution.
+//
+//   Glover diversification (include/ubqp.h ubqp_diversify)
+//   SplitMix64 random starts (include/ubqp.h ubqp_random)
+#include "ubqp_internal.cuh"
+
+namespace ubqp {
+namespace {
+
+// bits -> bytes: 4 bits of `nib` to 4 bytes (LSB first).  nib * (1 + 2^7 + 2^14 + 2^21)
+// places bit j at bit 8j with no two partial products overlapping, so no carries.
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) {
+    return (nib * 0x00204081u) & 0x01010101u;
+}
+
+__device__ __forceinline__ void store_expanded(int8_t *dst, uint64_t word) {
+    uint32_t o[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) o[i] = spread4(static_cast<uint32_t>(word >> (4 * i)) & 15u);
+    int4 *d = reinterpret_cast<int4 *>(dst);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        d[i] = make_int4(static_cast<int>(o[4 * i]), static_cast<int>(o[4 * i + 1]),
+                         static_cast<int>(o[4 * i + 2]), static_cast<int>(o[4 * i + 3]));
+}
+
+__device__ __forceinline__ uint64_t tail_mask(int n, int w) {
+    const int rem = n - 64 * w;
+    return rem >= 64 ? ~0ull : (rem <= 0 ? 0ull : ((1ull << rem) - 1ull));
+}
+
+// floor(sqrt(v)) for 0 <= v < 2^53, exact after correction
+__device__ __forceinline__ int64_t isqrt_dev(int64_t v) {
+    int64_t s = static_cast<int64_t>(sqrt(static_cast<double>(v)));
+    while (s * s > v) --s;
+    while ((s + 1) * (s + 1) <= v) ++s;
+    return s;
+}
+
+__global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict__ seed, int64_t t0,
+                                                     int64_t k, int rank, int world, int n,
+                                                     int W64, int NW, int n_pad,
+                                                     uint64_t *__restrict__ Xb,
+                                                     int8_t *__restrict__ X8) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= k * NW) return;
+    const int64_t slot = idx / NW;
+    const int w = static_cast<int>(idx - slot * NW);
+    uint64_t word = 0;
+    if (w < W64) {
+        const int64_t g = static_cast<int64_t>(rank) + slot * world;
+        const int64_t period = static_cast<int64_t>(n) * (n + 1);
+        int64_t t = (t0 + g) % period;
+        if (t < 0) t += period;
+        const int64_t h = (1 + isqrt_dev(1 + 4 * t)) / 2;
+        const int64_t r = t - h * (h - 1);
+        const int64_t q1 = r / 2;              // q - 1
+        const bool comp = (r & 1) != 0;
+        // M(h,q) restricted to [64w, 64w+64): j = q1 + m h
+        const int64_t lo = 64ll * w;
+        int64_t j = q1;
+        if (j < lo) j = q1 + ((lo - q1 + h - 1) / h) * h;
+        uint64_t mask = 0;
+        const int64_t hi = lo + 64 < n ? lo + 64 : n;
+        for (; j < hi; j += h) mask |= 1ull << (j - lo);
+        word = seed[w] ^ mask;
+        if (comp) word = ~word;
+        word &= tail_mask(n, w);
+        Xb[slot * W64 + w] = word;
+    }
+    store_expanded(X8 + slot * n_pad + 64ll * w, word);
+}
+
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) random_kernel(uint64_t seed, int64_t k, int rank, int world,
+                                                     int n, int W64, int NW, int n_pad,
+                                                     uint64_t *__restrict__ Xb,
+                                                     int8_t *__restrict__ X8) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= k * NW) return;
+    const int64_t slot = idx / NW;
+    const int w = static_cast<int>(idx - slot * NW);
+    uint64_t word = 0;
+    if (w < W64) {
+        const uint64_t g = static_cast<uint64_t>(rank) + static_cast<uint64_t>(slot) * world;
+        const uint64_t ctr = g * static_cast<uint64_t>(W64) + static_cast<uint64_t>(w) + 1ull;
+        word = splitmix_mix(seed + ctr * 0x9E3779B97F4A7C15ull) & tail_mask(n, w);
+        Xb[slot * W64 + w] = word;
+    }
+    store_expanded(X8 + slot * n_pad + 64ll * w, word);
+}
+
+__global__ void __launch_bounds__(256) expand_kernel(int64_t k, int n, int W64, int NW, int n_pad,
+                                                     uint64_t *__restrict__ Xb,
+                                                     int8_t *__restrict__ X8) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= k * NW) return;
+    const int64_t slot = idx / NW;
+    const int w = static_cast<int>(idx - slot * NW);
+    uint64_t word = 0;
+    if (w < W64) {
+        word = Xb[slot * W64 + w] & tail_mask(n, w);
+        Xb[slot * W64 + w] = word;
+    }
+    store_expanded(X8 + slot * n_pad + 64ll * w, word);
+}
+
+// x_i = [sum_j Q_ij > 0].  One warp per row i of Q8 (row sums fit int32: n*127).
+__global__ void __launch_bounds__(256) first_derivative_kernel(const int8_t *__restrict__ Q8, int n,
+                                                               int n_pad, int W64,
+                                                               uint32_t *__restrict__ bits32) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= 2 * W64) return;
+    // each warp owns one 32-bit output word: rows 32*warp .. 32*warp+31
+    uint32_t word = 0;
+    for (int r = 0; r < 32; ++r) {
+        const int i = warp * 32 + r;
+        int s = 0;
+        if (i < n)
+            for (int j = lane; j < n_pad; j += 32) s += Q8[static_cast<int64_t>(i) * n_pad + j];
+        s = __reduce_add_sync(0xffffffffu, s);
+        if (i < n && s > 0) word |= 1u << r;
+    }
+    if (lane == 0) bits32[warp] = word;
+}
+
+inline unsigned blocks_for(int64_t threads) { return static_cast<unsigned>((threads + 255) / 256); }
+
+}  // namespace
+
+void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k) {
+    if (k <= 0) return;
+    const int NW = c.n_pad / 64;
+    glover_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed_dev, t0, k, c.rank, c.world, c.n,
+                                                            c.W64, NW, c.n_pad, c.Xb, c.X8);
+    ++c.launches;
+}
+
+void launch_random(Ctx &c, uint64_t seed, int64_t k) {
+    if (k <= 0) return;
+    const int NW = c.n_pad / 64;
+    random_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed, k, c.rank, c.world, c.n, c.W64,
+                                                            NW, c.n_pad, c.Xb, c.X8);
+    ++c.launches;
+}
+
+void launch_expand(Ctx &c, int64_t k) {
+    if (k <= 0) return;
+    const int NW = c.n_pad / 64;
+    expand_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(k, c.n, c.W64, NW, c.n_pad, c.Xb, c.X8);
+    ++c.launches;
+}
+
+void launch_first_derivative(Ctx &c, uint64_t *bits_dev) {
+    const int warps = 2 * c.W64;   // one warp per 32-bit output word
+    first_derivative_kernel<<<(warps * 32 + 255) / 256, 256, 0, c.stream>>>(
+        c.Q8, c.n, c.n_pad, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
+    ++c.launches;
+}
+
+}  // namespace ubqp

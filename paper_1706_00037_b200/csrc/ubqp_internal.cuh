@@ -1,0 +1,217 @@
+// ubqp_internal.cuh — handle layout, launch declarations and sm_100a PTX helpers for
+// libubqp.so.  Not part of the ABI (include/ubqp.h is).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/ubqp.h"
+
+namespace ubqp {
+
+// ------------------------------------------------------------------ tiling constants
+constexpr int kBM = 128;          // eval tile rows (solutions) per CTA: UMMA M
+constexpr int kBN = 256;          // eval tile columns (variables j): UMMA N
+constexpr int kBK = 128;          // bytes of K (int8 elements) per pipeline stage = one 128B swizzle atom
+constexpr int kUmmaK = 32;        // K per tcgen05.mma kind::i8
+constexpr int kStages = 4;        // smem pipeline depth
+constexpr int kNPadAlign = 128;   // n_pad multiple (K dim of the GEMM)
+constexpr int kQRowAlign = kBN;   // Q8 rows padded to a multiple of the N tile
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    bool sticky_cuda = false;
+    std::string err;
+    int num_sms = 148;
+
+    // instance
+    int n = 0, n_pad = 0, q_rows = 0, W64 = 0;
+    int8_t *Q8 = nullptr;        // [q_rows][n_pad] row-major, zero padded; row k = column k (Q = Q^t)
+    int32_t *diag = nullptr;     // [q_rows]
+    uint64_t *seed = nullptr;    // [W64] staged diversification seed
+    // batch workspace
+    int64_t k_max = 0, k_cap_pad = 0, k_local = -1;
+    int rank = 0, world = 1;
+    uint64_t *Xb = nullptr;      // [k_max][W64] packed solutions
+    int8_t *X8 = nullptr;        // [k_cap_pad][n_pad] expanded 0/1 bytes (GEMM A operand)
+    int64_t *f = nullptr;        // [k_max] xQx of the batch
+    int32_t *gains = nullptr;    // [k_max][n_pad] 1-flip gains (lazy)
+    bool f_valid = false, gains_valid = false;
+    int32_t *surv = nullptr;     // [k_max]
+    int32_t *blk_count = nullptr;// screen block counts
+    int64_t *scratch64 = nullptr;// small device scratch (stats, m, best key)
+    // ascent outputs scratch
+    int64_t *asc_f = nullptr; int32_t *asc_flips = nullptr; uint64_t *asc_bits = nullptr;
+    int32_t *asc_slots = nullptr; int64_t asc_cap = 0;
+    // TMA descriptors (64 B each, passed by value as __grid_constant__)
+    CUtensorMap tmap_X8{}, tmap_Q8{};
+    int64_t launches = 0;
+};
+
+// ------------------------------------------------------------------ launchers (host)
+// gen.cu
+void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k);
+void launch_random(Ctx &c, uint64_t seed, int64_t k);
+void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
+void launch_first_derivative(Ctx &c, uint64_t *bits_dev);
+// eval_tc.cu
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains);
+void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev);
+// screen.cu
+void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);
+// ascend.cu
+int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,
+                  int64_t *f_dev, int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
+
+}  // namespace ubqp
+
+// ------------------------------------------------------------------ device helpers
+#ifdef __CUDACC__
+namespace ubqp {
+namespace dev {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    while (!mbar_try_wait(a, parity)) {
+    }
+}
+
+// ---- TMA
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap *m) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *m, int x, int y,
+                                            uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+// ---- tcgen05 (cta_group::1)
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, s8 x s8 -> s32
+__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns: thread (lane) l gets row (lane_base + l).
+__device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+}
+
+// UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, rows of 128 B,
+// 8-row core-matrix groups 1024 B apart (SBO), version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>(1u) << 16;             // LBO (unused for swizzled K-major)
+    d |= static_cast<uint64_t>(1024u >> 4) << 32;     // SBO
+    d |= static_cast<uint64_t>(1u) << 46;             // descriptor version (sm_100)
+    d |= static_cast<uint64_t>(2u) << 61;             // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor, kind::i8: D s32, A s8, B s8, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4)                                   // D format: S32
+           | (1u << 7)                                 // A: signed 8-bit
+           | (1u << 10)                                // B: signed 8-bit
+           | (static_cast<uint32_t>(N >> 3) << 17)     // N
+           | (static_cast<uint32_t>(M >> 4) << 24);    // M
+}
+
+}  // namespace dev
+}  // namespace ubqp
+#endif

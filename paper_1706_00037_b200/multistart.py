@@ -1,0 +1,172 @@
+"""One round of the diversified multi-start (Figure 2) over 1..N GPUs.
+
+torch is plumbing here: device buffers, the CUDA stream shared with libubqp.so, and
+torch.distributed (NCCL) for the only exchange steps of the method:
+  * the screening statistics {sum f, count, max_key} of the sharded batch (T uses
+    the Mean and Max over all solutions), and
+  * the best-record key (MAX) plus a broadcast of the winner's bits from its owner rank
+    (UpdateBestAndT).
+Solutions are sharded cyclically (slot i on rank r <-> g = r + i*world) and Q is
+replicated; every other step runs in the kernels behind include/ubqp.h.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .ubqp import UBQP_EMIT_GAINS, Ubqp
+
+KEY_SHIFT = 22
+F_OFFSET = 1 << 40
+
+
+def key_f(key: int) -> int:
+    """objective value stored in a max_key (include/ubqp.h)"""
+    return (int(key) >> KEY_SHIFT) - F_OFFSET
+
+
+def key_g(key: int) -> int:
+    """global solution index stored in a max_key"""
+    return (1 << KEY_SHIFT) - 1 - (int(key) & ((1 << KEY_SHIFT) - 1))
+
+
+def dist_info(group=None):
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+# ---------------------------------------------------------------- exchange steps (tested on gloo)
+def combine_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+    """stats int64[4] = {sum, count, max_key, 0} per rank -> global (SUM, SUM, MAX) in place."""
+    _, world = dist_info(group)
+    if world > 1:
+        sc = stats[:2].clone()
+        mk = stats[2:3].clone()
+        dist.all_reduce(sc, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(mk, op=dist.ReduceOp.MAX, group=group)
+        stats[:2].copy_(sc)
+        stats[2:3].copy_(mk)
+    return stats
+
+
+def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None):
+    """key int64[1] (rank-local best max_key, -1 = none), bits_row int64[W64] (that
+    solution's bits on its rank).  Returns (global key, winner bits) on every rank: MAX of
+    the keys, then a broadcast of the bits from the rank owning g = key_g (g mod world)."""
+    rank, world = dist_info(group)
+    if world == 1:
+        return int(key.item()), bits_row
+    gk = key.clone()
+    dist.all_reduce(gk, op=dist.ReduceOp.MAX, group=group)
+    k = int(gk.item())
+    if k < 0:
+        return k, bits_row
+    owner = key_g(k) % world
+    out = bits_row.clone()
+    src = dist.get_global_rank(group, owner) if group is not None else owner
+    dist.broadcast(out, src=src, group=group)
+    return k, out
+
+
+@dataclass
+class RoundResult:
+    m: int            # survivors on this rank
+    T: float          # screening value
+    best_key: int     # global best max_key of the ascended survivors (-1: none)
+    best_bits: torch.Tensor
+    batch_max: int
+    mean_sum: int
+    mean_count: int
+
+
+class MultiStart:
+    """Diversify -> eval(+gains) -> [all-reduce stats] -> screen -> ascend -> [best record]."""
+
+    def __init__(self, Q: np.ndarray, K: int, lam: float = 0.5, max_flips: int | None = None,
+                 device: int | None = None, group=None):
+        self.rank, self.world = dist_info(group)
+        self.group = group
+        self.device = torch.cuda.current_device() if device is None else device
+        self.n = int(Q.shape[0])
+        self.K = int(K)
+        self.k_local = len(range(self.rank, self.K, self.world))
+        self.lam = float(lam)
+        self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
+        self.u.load_Q(np.ascontiguousarray(Q, dtype=np.int32), max(self.k_local, 1))
+        self.W64 = self.u.W64
+        dv = torch.device("cuda", self.device)
+        kl = max(self.k_local, 1)
+        self.stats = torch.zeros(4, dtype=torch.int64, device=dv)
+        self.surv = torch.zeros(kl, dtype=torch.int32, device=dv)
+        self.f_asc = torch.zeros(kl, dtype=torch.int64, device=dv)
+        self.flips = torch.zeros(kl, dtype=torch.int32, device=dv)
+        self.bits = torch.zeros((kl, self.W64), dtype=torch.int64, device=dv)
+        self.key = torch.zeros(1, dtype=torch.int64, device=dv)
+        self.fd_bits = torch.zeros(self.W64, dtype=torch.int64, device=dv)
+
+    # CalculateFirstDerivativeSolution and its value (one-solution eval)
+    def first_derivative(self):
+        self.u.first_derivative(self.fd_bits)
+        self.u.set_batch(self.fd_bits, 1, 0, 1)
+        f = torch.zeros(1, dtype=torch.int64, device=self.fd_bits.device)
+        self.u.eval_batch(0, f)
+        return self.fd_bits.clone(), int(f.item())
+
+    # EvaluateRandomStarts: (sum, count) of K random solutions
+    def sample_mean(self, seed: int, K: int | None = None):
+        K = self.K if K is None else K
+        kl = len(range(self.rank, K, self.world))
+        self.u.random(seed, kl, self.rank, self.world)
+        self.u.eval_batch(0, None, self.stats)
+        combine_stats(self.stats, self.group)
+        s = self.stats.tolist()
+        return s[0], s[1]
+
+    def round(self, seed_bits: torch.Tensor, t0: int, inc_f: int, mean=None) -> RoundResult:
+        """One batched round.  mean=None -> the batch's own mean (R5)."""
+        u = self.u
+        u.diversify(seed_bits, t0, self.k_local, self.rank, self.world)
+        u.eval_batch(UBQP_EMIT_GAINS, None, self.stats)
+        combine_stats(self.stats, self.group)
+        ssum, scount, skey, _ = self.stats.tolist()
+        batch_max = key_f(skey)
+        mean_sum, mean_count = (ssum, scount) if mean is None else mean
+        maxv = max(inc_f, batch_max)
+        m, T = u.screen(self.lam, mean_sum, mean_count, maxv, self.surv)
+        u.ascend(self.surv, m, self.max_flips, self.f_asc, self.flips, self.bits, self.key)
+        row = self.bits[0]
+        if m > 0 and self.world > 1:
+            k_local = int(self.key.item())
+            if k_local >= 0 and key_g(k_local) % self.world == self.rank:
+                slot = (key_g(k_local) - self.rank) // self.world
+                i = int(torch.searchsorted(self.surv[:m], torch.tensor([slot], dtype=torch.int32,
+                                                                        device=self.surv.device)).item())
+                row = self.bits[i]
+        best_key, best_bits = combine_best(self.key, row.contiguous(), self.group)
+        if self.world == 1 and m > 0:
+            best_key = int(self.key.item())
+            slot = key_g(best_key)
+            i = int(torch.searchsorted(self.surv[:m], torch.tensor([slot], dtype=torch.int32,
+                                                                    device=self.surv.device)).item())
+            best_bits = self.bits[i].clone()
+        return RoundResult(m, T, best_key, best_bits, batch_max, mean_sum, mean_count)
+
+    def run(self, rounds: int, sample_seed: int, t_start: int = 0):
+        """Figure 2 as batched rounds (O8): pinned sampling mean, first-derivative
+        incumbent, rounds of diversify/eval/screen/ascend; strict improvement."""
+        mean = self.sample_mean(sample_seed)
+        inc_bits, inc_f = self.first_derivative()
+        traj = [(0, inc_f)]
+        for r in range(1, rounds + 1):
+            res = self.round(inc_bits, t_start + (r - 1) * self.K, inc_f, mean)
+            if res.best_key >= 0 and key_f(res.best_key) > inc_f:
+                inc_f = key_f(res.best_key)
+                inc_bits = res.best_bits.clone()
+                traj.append((r, inc_f))
+        return inc_f, inc_bits, traj

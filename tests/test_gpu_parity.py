@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Integer Q => every comparison is exact (north_star "bit-exact").
+Sizes span several tiles and ragged tails: n in {1..129, 500, 1100, 2500} crosses the
+128-byte K block, the 256-column N tile and the 64-bit word; K crosses the 128-row M
+tile.  Full-size (n = 7000, K = 262144) runs compare sampled rows.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import generate_Q, pack_bits, unpack_bits
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp, UbqpError, ubqp_stats  # noqa: E402
+from paper_1706_00037_b200.build import build_lib  # noqa: E402
+
+build_lib()
+
+NS = [1, 2, 3, 31, 50, 63, 64, 65, 127, 128, 129, 257, 500, 1100, 2500]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    return Ubqp(0)
+
+
+def _handle_with(Q, k_max):
+    u = Ubqp(0)
+    u.load_Q(Q, k_max)
+    return u
+
+
+def _batch(u, K, n):
+    B = np.zeros((max(K, 1), u.W64), dtype=np.uint64)
+    u.get_batch(B)
+    return unpack_bits(B[:K], n)
+
+
+@pytest.mark.parametrize("n", NS)
+def test_random_batch_bits(n):
+    Q = generate_Q(n, 0.5, seed=n)
+    K = 300
+    u = _handle_with(Q, K)
+    u.random(1234 + n, K)
+    assert np.array_equal(_batch(u, K, n), oracle.random_solutions(n, 1234 + n, K))
+
+
+@pytest.mark.parametrize("n", NS)
+def test_glover_batch_bits(n):
+    Q = generate_Q(n, 0.5, seed=n)
+    K = 333
+    rng = np.random.default_rng(n)
+    seed_x = rng.integers(0, 2, size=n).astype(np.uint8)
+    u = _handle_with(Q, K)
+    for t0 in (0, 5 * n * (n + 1) + 17):
+        u.diversify(pack_bits(seed_x)[0], t0, K)
+        assert np.array_equal(_batch(u, K, n), oracle.diversify(seed_x, t0, K)), t0
+
+
+@pytest.mark.parametrize("n", NS)
+@pytest.mark.parametrize("density", [0.1, 1.0])
+def test_eval_f_and_stats(n, density):
+    Q = generate_Q(n, density, seed=7 * n + 1)
+    K = 1 if n == 1 else 389                       # 4 M tiles, ragged
+    u = _handle_with(Q, 512)
+    u.random(99, K)
+    f = np.zeros(K, dtype=np.int64)
+    st = ubqp_stats()
+    u.eval_batch(0, f, st)
+    X = oracle.random_solutions(n, 99, K)
+    ref = oracle.eval_batch(Q, X, nthreads=8)
+    assert np.array_equal(f, ref)
+    ost = oracle.stats(ref)
+    assert (st.sum, st.count, st.max_key, st.reserved) == tuple(int(v) for v in ost)
+
+
+@pytest.mark.parametrize("n", [1, 3, 65, 129, 500, 1100])
+def test_eval_gains(n):
+    Q = generate_Q(n, 0.7, seed=n + 3)
+    K = 150
+    u = _handle_with(Q, K)
+    u.random(5, K)
+    f = np.zeros(K, dtype=np.int64)
+    u.eval_batch(UBQP_EMIT_GAINS, f)
+    G = np.zeros((K, n), dtype=np.int32)
+    u.get_gains(0, K, G)
+    X = oracle.random_solutions(n, 5, K)
+    for k in range(0, K, 7 if n > 500 else 1):
+        assert np.array_equal(G[k].astype(np.int64), oracle.gains(Q, X[k])), k
+    assert np.array_equal(f, oracle.eval_batch(Q, X, nthreads=8))
+
+
+def test_eval_device_pointers_torch():
+    n, K = 700, 600
+    Q = generate_Q(n, 0.3, seed=11)
+    u = Ubqp(0, stream=torch.cuda.current_stream().cuda_stream)
+    u.load_Q(torch.from_numpy(Q).cuda(), K)
+    bits = torch.from_numpy(pack_bits(oracle.random_solutions(n, 8, K)).view(np.int64)).cuda()
+    u.set_batch(bits, K)
+    f = torch.zeros(K, dtype=torch.int64, device="cuda")
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    u.eval_batch(0, f, st)
+    torch.cuda.synchronize()
+    ref = oracle.eval_batch(Q, oracle.random_solutions(n, 8, K), nthreads=8)
+    assert np.array_equal(f.cpu().numpy(), ref)
+    assert st.cpu().tolist() == oracle.stats(ref).tolist()
+
+
+@pytest.mark.parametrize("lam", [0.0, 0.25, 0.5, 0.9, 1.0, -0.3])
+def test_screen(lam):
+    n, K = 300, 5000
+    Q = generate_Q(n, 0.5, seed=21)
+    u = _handle_with(Q, K)
+    u.random(3, K)
+    f = np.zeros(K, dtype=np.int64)
+    st = ubqp_stats()
+    u.eval_batch(0, f, st)
+    maxv = (st.max_key >> 22) - (1 << 40)
+    surv = np.zeros(K, dtype=np.int32)
+    m, T = u.screen(lam, st.sum, st.count, maxv, surv)
+    To = oracle.threshold(lam, st.sum, st.count, maxv)
+    assert T == To
+    assert np.array_equal(surv[:m], oracle.screen(f, To))
+
+
+def test_screen_boundary_equal_fails():
+    n = 2
+    Q = np.array([[1, 2], [2, -3]], dtype=np.int32)
+    u = _handle_with(Q, 4)
+    u.set_batch(pack_bits(np.array([[0, 0], [1, 0], [1, 1], [0, 1]], np.uint8)), 4)
+    f = np.zeros(4, dtype=np.int64)
+    u.eval_batch(0, f)
+    assert f.tolist() == [0, 1, 2, -3]
+    surv = np.zeros(4, dtype=np.int32)
+    m, T = u.screen(0.5, 0, 1, 2, surv)           # T = 1: f = 1 does not pass ("exceeds")
+    assert T == 1.0 and surv[:m].tolist() == [2]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 50, 129, 500, 1100, 2500])
+@pytest.mark.parametrize("max_flips", [0, 3, 100000])
+def test_ascend(n, max_flips):
+    Q = generate_Q(n, 0.8, seed=31 + n)
+    K = 64 if n >= 1100 else 200
+    u = _handle_with(Q, K)
+    u.random(17, K)
+    u.eval_batch(UBQP_EMIT_GAINS)
+    slots = np.arange(0, K, 3, dtype=np.int32)[::-1].copy()   # unordered subset
+    m = len(slots)
+    f_o = np.zeros(m, np.int64)
+    fl_o = np.zeros(m, np.int32)
+    b_o = np.zeros((m, u.W64), np.uint64)
+    key = np.zeros(1, np.int64)
+    u.ascend(slots, m, max_flips, f_o, fl_o, b_o, key)
+    X0 = oracle.random_solutions(n, 17, K)[slots]
+    Xr, fr, flr = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0), max_flips, nthreads=8)
+    assert np.array_equal(unpack_bits(b_o, n), Xr)
+    assert np.array_equal(f_o, fr)
+    assert np.array_equal(fl_o, flr)
+    best = max(oracle.max_key(int(fr[i]), int(slots[i])) for i in range(m))
+    assert key[0] == best
+
+
+def test_ascend_computes_missing_gains_and_empty():
+    n, K = 300, 100
+    Q = generate_Q(n, 0.5, seed=2)
+    u = _handle_with(Q, K)
+    u.random(4, K)
+    u.eval_batch(0)                               # no gains: ascend must compute them
+    f_o = np.zeros(K, np.int64)
+    u.ascend(np.arange(K, dtype=np.int32), K, 10 * n, f_o)
+    X0 = oracle.random_solutions(n, 4, K)
+    _, fr, _ = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0), 10 * n, nthreads=8)
+    assert np.array_equal(f_o, fr)
+    key = np.zeros(1, np.int64)
+    u.ascend(np.zeros(1, np.int32), 0, 10, best_key_out=key)
+    assert key[0] == -1
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharding_matches_single_rank(world):
+    n, K = 400, 1000
+    Q = generate_Q(n, 0.5, seed=5)
+    seed_x = np.random.default_rng(1).integers(0, 2, size=n).astype(np.uint8)
+    full = oracle.eval_batch(Q, oracle.diversify(seed_x, 3, K), nthreads=8)
+    u = _handle_with(Q, K)
+    tot = 0
+    best = -1
+    for r in range(world):
+        kr = len(range(r, K, world))
+        u.diversify(pack_bits(seed_x)[0], 3, kr, r, world)
+        f = np.zeros(kr, np.int64)
+        st = ubqp_stats()
+        u.eval_batch(0, f, st)
+        assert np.array_equal(f, full[r::world])
+        tot += st.sum
+        best = max(best, st.max_key)
+    ost = oracle.stats(full)
+    assert tot == ost[0] and best == ost[2]
+
+
+def test_first_derivative_start():
+    for n in (3, 64, 65, 1000):
+        Q = generate_Q(n, 0.5, seed=n)
+        u = _handle_with(Q, 4)
+        b = np.zeros(u.W64, np.uint64)
+        u.first_derivative(b)
+        assert np.array_equal(unpack_bits(b, n)[0], oracle.first_derivative_start(Q))
+
+
+def test_errors():
+    u = Ubqp(0)
+    with pytest.raises(UbqpError) as e:
+        u.eval_batch(0)
+    assert e.value.code == 4                       # E_STATE
+    Q = np.array([[1, 2], [3, 1]], np.int32)
+    with pytest.raises(UbqpError) as e:
+        u.load_Q(Q, 4)
+    assert e.value.code == 2                       # E_NOT_SYMMETRIC
+    with pytest.raises(UbqpError) as e:
+        u.load_Q(np.array([[200]], np.int32), 4)
+    assert e.value.code == 3                       # E_RANGE
+    u.load_Q(np.array([[5]], np.int32), 4)
+    with pytest.raises(UbqpError):
+        u.random(0, 5)                             # k_local > k_max
+    u.random(0, 0)
+    st = ubqp_stats()
+    u.eval_batch(0, None, st)
+    assert st.count == 0 and st.max_key == -1
+
+
+# ------------------------------------------------------------------ full-size, sampled
+@pytest.mark.parametrize("n,K,kind", [(5000, 1000, "random"), (7000, 1000, "random"),
+                                      (7000, 262144, "glover")])
+def test_full_size_sampled(n, K, kind):
+    Q = generate_Q(n, 1.0, seed=4)
+    u = _handle_with(Q, K)
+    if kind == "random":
+        u.random(4, K)
+        Xs = lambda idx: oracle.random_solutions(n, 4, K)[idx]   # noqa: E731
+    else:
+        b = np.zeros(u.W64, np.uint64)
+        u.first_derivative(b)
+        seed_x = unpack_bits(b, n)[0]
+        u.diversify(b, 0, K)
+        Xs = lambda idx: np.stack([oracle.diversify(seed_x, int(i), 1)[0] for i in idx])  # noqa: E731
+    f = np.zeros(K, np.int64)
+    st = ubqp_stats()
+    u.eval_batch(0, f, st)
+    rng = np.random.default_rng(0)
+    idx = np.unique(np.concatenate([[0, 1, K - 1], rng.integers(0, K, 61)]))
+    assert np.array_equal(f[idx], oracle.eval_batch(Q, Xs(idx), nthreads=8))
+    assert st.sum == int(f.sum()) and st.count == K
