@@ -1,0 +1,416 @@
+#!/usr/bin/env python
+"""Benchmark of the UBQP multi-start hot path on B200 (contract: see DESIGN.md §8).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one full round of the method (Figure 2) over one batch:
+    Glover diversify -> xQx eval + 1-flip gains (tcgen05 int8) -> stats all-reduce ->
+    T(lambda) screen -> batched steepest ascent of the survivors -> best record,
+on BASELINE.json config 4: n = 7000 dense integer Q (U{-100..100}\\{0}, seed 4),
+K = 262144 Glover solutions from the first-derivative start (t0 = 0), lambda = 0.5,
+max_flips = 10 n, sharded cyclically over the ranks (strong scaling).
+value = K / (step time, max over ranks) in xQx evals/s.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from inputs import CONFIGS, generate_Q  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+METRIC = "xQx evals/sec (full diversify-eval-screen-ascent round)"
+UNIT = "evals/s"
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["_source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["_source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+def workload_config(cfg, world, extra=None):
+    c = {"workload": cfg["name"], "n": cfg["n"], "density": cfg["density"], "seed_Q": cfg["seed_Q"],
+         "K_global": cfg["K"], "K_per_rank": len(range(0, cfg["K"], world)), "lambda": cfg.get("lam"),
+         "max_flips": cfg.get("max_flips"), "t0": 0, "Q_coeffs": "U{-100..100}\\{0}",
+         "parallelism": f"dp{world} (solutions sharded cyclically, Q replicated)",
+         "l2": "inputs larger than L2 (X8 1.85 GB + gains 7.4 GB per round); Q (49 MB) L2-resident by design"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period: float = 0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.ok = False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "note": "nvml unavailable"}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ oracle (cpu_baseline / reference arm)
+def oracle_sample_step(Q, x0, f0, cfg, S, threads):
+    """The oracle doing one bounded sample of the workload: the first S slots of the batch
+    (eval + screen against the sample's own mean/max + ascent of the survivors)."""
+    import oracle
+    X = oracle.diversify(x0, 0, S)
+    f = oracle.eval_batch(Q, X, threads)
+    maxv = max(f0, int(f.max()))
+    T = oracle.threshold(cfg["lam"], int(f.sum()), S, maxv)
+    s = oracle.screen(f, T)
+    _, fa, flips = oracle.ascend(Q, X[s], f[s], cfg["max_flips"], threads)
+    return len(s), int(flips.sum())
+
+
+def cpu_sample_size(Q, x0, f0, cfg, cores, target_s):
+    """Size the bounded oracle sample so one step costs about target_s seconds of CPU time."""
+    if "UBQP_CPU_SAMPLE" in os.environ:
+        return int(os.environ["UBQP_CPU_SAMPLE"])
+    S = cores
+    t = time.perf_counter()
+    oracle_sample_step(Q, x0, f0, cfg, S, cores)
+    dt = max(time.perf_counter() - t, 1e-3)
+    S = int(S * target_s / dt) // cores * cores
+    return max(cores, min(S, cfg["K"]))
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    import oracle
+    cores = os.cpu_count() or 1
+    Q = generate_Q(cfg["n"], cfg["density"], seed=cfg["seed_Q"])
+    x0 = oracle.first_derivative_start(Q)
+    f0 = oracle.xQx(Q, x0)
+    S = cpu_sample_size(Q, x0, f0, cfg, cores, target_s=8.0)
+    for _ in range(args.warmup):
+        oracle_sample_step(Q, x0, f0, cfg, S, cores)
+    t = time.perf_counter()
+    tot_flips = 0
+    for _ in range(args.steps):
+        _, fl = oracle_sample_step(Q, x0, f0, cfg, S, cores)
+        tot_flips += fl
+    dt = time.perf_counter() - t
+    value = S * args.steps / dt
+    sample = (f"first {S} of the {cfg['K']} Glover solutions per step (eval + screen + ascent of "
+              f"survivors), {cores} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic", "config": workload_config(cfg, 1, {"sample_per_step": S}),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ascent_flips_per_step": tot_flips / args.steps,
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_00037_b200 import UBQP_EMIT_GAINS
+    from paper_1706_00037_b200.build import build_lib
+    from paper_1706_00037_b200.multistart import MultiStart, combine_stats, key_f
+
+    build_lib()
+    torch.cuda.set_device(local_rank)
+    peaks = load_peaks()
+    n, K, lam = cfg["n"], cfg["K"], cfg["lam"]
+    Q = generate_Q(n, cfg["density"], seed=cfg["seed_Q"])
+    ms = MultiStart(Q, K, lam=lam, max_flips=cfg["max_flips"], device=local_rank)
+    u = ms.u
+    stream = ms.stream
+    x0_bits, f0 = ms.first_derivative()
+
+    ev = {k: torch.cuda.Event(enable_timing=True) for k in
+          ("eval0", "eval1", "asc0", "asc1")}
+    acc = {"eval": 0.0, "asc": 0.0}
+
+    def step(timed_kernels: bool):
+        u.diversify(x0_bits, 0, ms.k_local, rank, world)
+        if timed_kernels:
+            ev["eval0"].record(stream)
+        u.eval_batch(UBQP_EMIT_GAINS, None, ms.stats)
+        if timed_kernels:
+            ev["eval1"].record(stream)
+        combine_stats(ms.stats)
+        ssum, scount, skey, _ = ms.stats.tolist()
+        maxv = max(f0, key_f(skey))
+        m, T = u.screen(lam, ssum, scount, maxv, ms.surv)
+        if timed_kernels:
+            ev["asc0"].record(stream)
+        u.ascend(ms.surv, m, ms.max_flips, ms.f_asc, ms.flips, ms.bits, ms.key)
+        if timed_kernels:
+            ev["asc1"].record(stream)
+        gk = ms.key.clone()
+        if world > 1:
+            dist.all_reduce(gk, op=dist.ReduceOp.MAX)
+        if timed_kernels:
+            stream.synchronize()
+            acc["eval"] += ev["eval0"].elapsed_time(ev["eval1"])
+            acc["asc"] += ev["asc0"].elapsed_time(ev["asc1"])
+        return m, int(gk.item())
+
+    for _ in range(args.warmup):
+        m, gkey = step(False)
+    flips_total = int(ms.flips[:m].sum().item()) if m else 0
+    launches0 = u.launches
+
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            m, gkey = step(True)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = u.launches - launches0
+    ms_step = t_start.elapsed_time(t_end) / args.steps
+    eval_ms = acc["eval"] / args.steps
+    asc_ms = acc["asc"] / args.steps
+    t = torch.tensor([ms_step, eval_ms, asc_ms, float(flips_total), float(m)], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_step, eval_ms, asc_ms = tmax[0].item(), tmax[1].item(), tmax[2].item()
+        flips_all, m_all = tsum[3].item(), tsum[4].item()
+    else:
+        flips_all, m_all = float(flips_total), float(m)
+
+    # ---- e2e through the C-ABI with host (pinned) buffers, copies inside the timed region
+    kl = ms.k_local
+    W = ms.W64
+    h_seed = torch.empty(W, dtype=torch.int64, pin_memory=True)
+    h_seed.copy_(x0_bits.cpu())
+    h_stats = torch.empty(4, dtype=torch.int64, pin_memory=True)
+    h_surv = torch.empty(max(kl, 1), dtype=torch.int32, pin_memory=True)
+    h_f = torch.empty(max(kl, 1), dtype=torch.int64, pin_memory=True)
+    h_fl = torch.empty(max(kl, 1), dtype=torch.int32, pin_memory=True)
+    h_bits = torch.empty((max(kl, 1), W), dtype=torch.int64, pin_memory=True)
+    h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    e_steps = max(1, min(args.steps, 3))
+    d_stats = ms.stats
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d = d2h = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e_steps):
+        u.diversify(h_seed, 0, kl, rank, world)
+        u.eval_batch(UBQP_EMIT_GAINS, None, h_stats)
+        if world > 1:
+            d_stats.copy_(h_stats, non_blocking=False)
+            combine_stats(d_stats)
+            h_stats.copy_(d_stats)
+        s = h_stats.tolist()
+        m_e, T_e = u.screen(lam, s[0], s[1], max(f0, key_f(s[2])), h_surv)
+        u.ascend(h_surv, m_e, ms.max_flips, h_f, h_fl, h_bits, h_key)
+        h2d += W * 8 + m_e * 4
+        d2h += 32 + m_e * 4 + m_e * (8 + 4 + W * 8) + 8
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / e_steps
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = te.item()
+
+    if rank != 0:
+        return
+    value = K / (ms_step * 1e-3)
+    # ---- roofline of the dominant kernel (achieved from live CUDA events of this run)
+    eval_ops = 2.0 * n * n * K / world                       # per rank per launch (algorithmic)
+    eval_tops = eval_ops / (eval_ms * 1e-3) / 1e12
+    int8_peak_burst = 2.0 * peaks["bf16_tflops"]             # guide: int8 dense = 2x bf16 nominal
+    int8_peak_sust = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    asc_bytes = flips_all / world * n                        # one int8 Q row per flip step
+    asc_gbs = asc_bytes / (asc_ms * 1e-3) / 1e9 if asc_ms > 0 else 0.0
+    traffic = {}
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(cfg["name"], {})
+        except Exception:
+            traffic = {}
+    roof_eval = {"bound": "tensor", "achieved": eval_tops, "peak": int8_peak_sust, "unit": "TOP/s",
+                 "frac": eval_tops / int8_peak_sust, "traffic": traffic.get("eval_tc_kernel"),
+                 "kernel": "eval_tc_kernel (+stats)", "ms": eval_ms,
+                 "peak_note": f"int8 = 2 x bf16 {peaks['_source']} sustained; burst peak {int8_peak_burst:.0f}",
+                 "frac_of_burst": eval_tops / int8_peak_burst, "frac_of_spec_4500": eval_tops / 4500.0}
+    roof_asc = {"bound": "hbm", "achieved": asc_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": asc_gbs / peaks["hbm_gbs"], "traffic": traffic.get("ascend_kernel"),
+                "kernel": "ascend_kernel", "ms": asc_ms, "steps_per_s": flips_all / (asc_ms * 1e-3) if asc_ms else 0,
+                "algorithmic_bytes": "n bytes (one int8 Q row) per flip step"}
+    dominant = roof_asc if asc_ms >= eval_ms else roof_eval
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "int8xint8->int32 eval, int32/int64 ascent", "data": "synthetic",
+        "config": workload_config(cfg, world),
+        "roofline": dominant,
+        "roofline_eval": roof_eval, "roofline_ascent": roof_asc,
+        "eval_only_evals_per_s": K / (eval_ms * 1e-3),
+        "survivors_per_step": m_all, "flip_steps_per_step": flips_all,
+        "e2e": {"value": K / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // e_steps,
+                "d2h_bytes_per_step": d2h // e_steps, "ms_per_step": e2e_ms,
+                "path": "C-ABI with pinned host buffers (seed in; stats, survivors, ascent outputs out)"},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, Q)
+    if world == 1 and not args.no_table1:
+        out["table1_eval_1000"] = table1_eval(local_rank)
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(cfg, Q):
+    import oracle
+    cores = os.cpu_count() or 1
+    x0 = oracle.first_derivative_start(Q)
+    f0 = oracle.xQx(Q, x0)
+    S = cpu_sample_size(Q, x0, f0, cfg, cores, target_s=15.0)
+    t = time.perf_counter()
+    m, fl = oracle_sample_step(Q, x0, f0, cfg, S, cores)
+    dt = time.perf_counter() - t
+    return {"value": S / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {S} of the {cfg['K']} Glover solutions (eval + screen + ascent of {m} "
+                      f"survivors, {fl} flips), {cores} threads, {dt:.1f} s"}
+
+
+def table1_eval(device):
+    """Paper Table 1 shape: 1000 random solutions evaluated at n = 2500/5000/7000."""
+    import torch
+
+    from paper_1706_00037_b200 import Ubqp
+    res = {}
+    for n, dens, sq, paper_s in ((2500, 0.1, 2, 0.7), (5000, 1.0, 3, 2.0), (7000, 1.0, 4, 3.5)):
+        Q = generate_Q(n, dens, seed=sq)
+        u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+        u.load_Q(Q, 1000)
+        u.random(sq, 1000)
+        f = torch.zeros(1000, dtype=torch.int64, device="cuda")
+        st = torch.zeros(4, dtype=torch.int64, device="cuda")
+        for _ in range(5):
+            u.eval_batch(0, f, st)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        e0.record()
+        for _ in range(reps):
+            u.eval_batch(0, f, st)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / reps * 1e3
+        res[f"n{n}"] = {"us_per_1000_evals": us, "evals_per_s": 1000 / (us * 1e-6),
+                        "paper_gtx780ti_s": paper_s, "speedup_vs_paper": paper_s / (us * 1e-6)}
+        u.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-table1", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: the contract requires >= 3 warm-up steps", file=sys.stderr)
+    key = int(args.config) if args.config.isdigit() else args.config
+    cfg = dict(CONFIGS[key])
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

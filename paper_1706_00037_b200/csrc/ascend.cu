@@ -7,11 +7,18 @@
 //     f += Delta_k*;  d = 1 - 2 x_k*;  x_k* ^= 1;
 //     Delta_j += 2 d (1 - 2 x_j) Q_{j k*}  (j != k*);   Delta_k* = -Delta_k*.
 //
-// One CTA per survivor.  The gain vector lives in registers: thread t owns the 4
-// consecutive variables j = c*4*BLOCK + 4t + e (e < 4) of every chunk c < NCH, so each
-// step streams row k* of Q8 (= column k* by symmetry, n bytes, coalesced 4 B per thread)
-// exactly once.  The argmax is a warp __reduce_max/__reduce_min pair plus one
-// __syncthreads over double-buffered shared slots; x_k* travels with the winning index.
+// One CTA of BLOCK threads per survivor; thread t owns the 16 consecutive variables
+// j = c*16*BLOCK + 16t + e (e < 16) of every chunk c < NCH, so a step streams row k* of
+// Q8 (= column k*, Q symmetric; n bytes) with one 16-byte load per chunk.  Each gain is
+// held in a register as a totally ordered key
+//     K_j = 256 Delta_j + 2 (127 - li) + x_j          (li = 16c + e, the local index)
+// so the running argmax (largest Delta, then lowest j) is one IMNMX per element and the
+// update is one IMAD with a block-uniform multiplier C = 512 d applied to the byte
+// s_j Q_{k* j}; the per-variable sign s_j = 1 - 2 x_j is applied to 4 packed bytes at once
+// (x is held as byte masks).  Per element and step: PRMT + IMAD + IMNMX + 1/4 of the
+// packed sign fix-up.  The owner of k* pre-compensates K_k* through a jump table so the
+// fused loop needs no per-element test.  Argmax across lanes: __reduce_max/min_sync;
+// across warps: one __syncthreads over double-buffered shared slots.
 #include <climits>
 
 #include "ubqp_internal.cuh"
@@ -19,19 +26,72 @@
 namespace ubqp {
 namespace {
 
+constexpr int kPad = -(1 << 30);     // key of padding variables: below every real key
+
+__device__ __forceinline__ int sext_byte(uint32_t w, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, %2;" : "=r"(r) : "r"(w), "r"(sel));
+    return static_cast<int>(r);
+}
+// selector: byte b in the low byte, its sign replicated above
+__device__ __forceinline__ constexpr uint32_t sel_of(int b) {
+    return static_cast<uint32_t>(b) | ((8u | b) << 4) | ((8u | b) << 8) | ((8u | b) << 12);
+}
+// negate the bytes of w selected by mask m (0xFF per negated byte), no carries across bytes
+__device__ __forceinline__ uint32_t neg_bytes(uint32_t w, uint32_t m) {
+    const uint32_t t = w ^ m;
+    return ((t & 0x7F7F7F7Fu) + (m & 0x01010101u)) ^ (t & 0x80808080u);
+}
+__device__ __forceinline__ uint32_t byte_mask_of_nibble(uint32_t nib) {
+    return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
+}
+__device__ __forceinline__ uint32_t nibble_of_byte_mask(uint32_t m) {
+    return (((m & 0x01010101u) * 0x01020408u) >> 24) & 0xFu;
+}
+__device__ __forceinline__ uint32_t word_of(const uint4 &v, int i) {
+    return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
 template <int BLOCK, int NCH>
-__global__ void __launch_bounds__(BLOCK)
-ascend_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n, int n_pad,
-              int W64, int64_t k_local, int rank, int world, const int8_t *__restrict__ Q8,
+struct Asc {
+    static constexpr int E = 16 * NCH;      // variables per thread
+    static constexpr int CHUNK = 16 * BLOCK;
+    static constexpr int NW = BLOCK / 32;
+};
+
+// Owner of k*: pre-set K so that after the uniform update (+C s_new q_kk = -512 q_kk) it
+// equals 256(-Delta_old) + 2(127 - li) + x_new, and flip x's byte mask.
+template <int L, int NCH>
+__device__ __forceinline__ void owner_fix(int (&K)[NCH][16], uint32_t (&m)[NCH][4],
+                                          const uint4 (&w)[NCH], int gv, int x_new) {
+    constexpr int c = L >> 4, e = L & 15, wi = e >> 2, b = e & 3;
+    if constexpr (c < NCH) {
+        const int qkk = sext_byte(word_of(w[c], wi), sel_of(b));
+        K[c][e] = -gv * 256 + 2 * (127 - L) + x_new + 512 * qkk;
+        m[c][wi] ^= 0xFFu << (8 * b);
+    }
+}
+
+#define UBQP_CASE(L) \
+    case L:          \
+        owner_fix<L, NCH>(K, m, w, gv, x_new); \
+        break;
+#define UBQP_CASE8(B) UBQP_CASE(B) UBQP_CASE(B + 1) UBQP_CASE(B + 2) UBQP_CASE(B + 3) \
+                      UBQP_CASE(B + 4) UBQP_CASE(B + 5) UBQP_CASE(B + 6) UBQP_CASE(B + 7)
+
+template <int BLOCK, int NCH, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int W64,
+              int64_t k_local, int rank, int world, const int8_t *__restrict__ Q8,
               const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
               const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out,
               int32_t *__restrict__ flips_out, uint64_t *__restrict__ bits_out,
               long long *__restrict__ best_key) {
-    constexpr int NW = BLOCK / 32;
-    constexpr int CH = 4 * BLOCK;   // variables per chunk
-    __shared__ int s_val[2][NW];
-    __shared__ unsigned s_idx[2][NW];
-    __shared__ uint32_t s_bits[(CH * NCH) / 32];
+    using A = Asc<BLOCK, NCH>;
+    static_assert(A::E <= 128, "local index must fit 7 bits");
+    __shared__ int s_val[2][A::NW];
+    __shared__ unsigned s_key[2][A::NW];
+    __shared__ uint32_t s_bits[(A::CHUNK * NCH) / 32];
 
     const int i = blockIdx.x;
     const int t = threadIdx.x;
@@ -45,101 +105,138 @@ ascend_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n
         return;
     }
 
-    int32_t D[NCH][4];
-    uint32_t xm = 0;                            // bit (4c + e) = x_j
+    int K[NCH][16];
+    uint32_t m[NCH][4];
     const int32_t *grow = gains + s * n_pad;
     const uint64_t *xrow = Xb + s * W64;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
-        const int j0 = c * CH + 4 * t;
-        if (j0 < n_pad) {
-            const int4 v = *reinterpret_cast<const int4 *>(grow + j0);
-            D[c][0] = v.x; D[c][1] = v.y; D[c][2] = v.z; D[c][3] = v.w;
-        } else {
-            D[c][0] = D[c][1] = D[c][2] = D[c][3] = INT_MIN;
-        }
-        uint32_t b4 = 0;
-        if (j0 < n) b4 = static_cast<uint32_t>(xrow[j0 >> 6] >> (j0 & 63)) & 15u;
-        xm |= b4 << (4 * c);
+        const int j0 = c * A::CHUNK + 16 * t;
+        uint32_t bits16 = 0;
+        if (j0 < n) bits16 = static_cast<uint32_t>(xrow[j0 >> 6] >> (j0 & 63)) & 0xFFFFu;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (j0 + e >= n) D[c][e] = INT_MIN;    // padding is never a candidate
+        for (int wi = 0; wi < 4; ++wi) m[c][wi] = byte_mask_of_nibble((bits16 >> (4 * wi)) & 15u);
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+            int4 g = make_int4(0, 0, 0, 0);
+            if (j0 < n_pad) g = *reinterpret_cast<const int4 *>(grow + j0 + 4 * q4);
+            const int gg[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int e = 4 * q4 + b;
+                const int li = 16 * c + e;
+                K[c][e] = (j0 + e < n) ? gg[b] * 256 + 2 * (127 - li) + static_cast<int>((bits16 >> e) & 1u)
+                                       : kPad;
+            }
+        }
     }
+    int run = kPad;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) run = max(run, K[c][e]);
+
     int64_t fv = f_in[s];
     int flips = 0;
     int par = 0;
-
     for (;;) {
-        // ---- argmax with lowest-index tie-break; carry x_k* in bit 0 of the index key
-        int bv = INT_MIN;
-        unsigned bk = 0xFFFFFFFFu;
-#pragma unroll
-        for (int c = 0; c < NCH; ++c)
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (D[c][e] > bv) {                // strict: first (lowest) j wins ties
-                    bv = D[c][e];
-                    bk = (static_cast<unsigned>(c * CH + 4 * t + e) << 1) | ((xm >> (4 * c + e)) & 1u);
-                }
-        const int wv = __reduce_max_sync(0xFFFFFFFFu, bv);
-        const unsigned wk = __reduce_min_sync(0xFFFFFFFFu, bv == wv ? bk : 0xFFFFFFFFu);
-        if (lane == 0) {
-            s_val[par][warp] = wv;
-            s_idx[par][warp] = wk;
+        // ---- argmax: lane -> warp (max Delta, then min j) -> block
+        const int dv = run >> 8;
+        const int wv = __reduce_max_sync(0xFFFFFFFFu, dv);
+        unsigned cand = 0xFFFFFFFFu;
+        if (dv == wv) {
+            const int li = 127 - ((run >> 1) & 127);
+            const int j = (li >> 4) * A::CHUNK + 16 * t + (li & 15);
+            cand = (static_cast<unsigned>(j) << 1) | static_cast<unsigned>(run & 1);
         }
-        __syncthreads();
-        int gv = s_val[par][0];
-        unsigned gk = s_idx[par][0];
+        const unsigned wk = __reduce_min_sync(0xFFFFFFFFu, cand);
+        int gv;
+        unsigned gk;
+        if constexpr (A::NW == 1) {
+            gv = wv;
+            gk = wk;
+        } else {
+            if (lane == 0) {
+                s_val[par][warp] = wv;
+                s_key[par][warp] = wk;
+            }
+            __syncthreads();
+            gv = s_val[par][0];
+            gk = s_key[par][0];
 #pragma unroll
-        for (int w = 1; w < NW; ++w) {
-            const int v = s_val[par][w];
-            const unsigned k = s_idx[par][w];
-            if (v > gv || (v == gv && k < gk)) { gv = v; gk = k; }
+            for (int w2 = 1; w2 < A::NW; ++w2) {
+                const int v = s_val[par][w2];
+                const unsigned k2 = s_key[par][w2];
+                if (v > gv || (v == gv && k2 < gk)) { gv = v; gk = k2; }
+            }
+            par ^= 1;
         }
-        par ^= 1;
         if (gv <= 0 || flips == max_flips) break;
 
-        // ---- apply the flip of k*
+        // ---- flip k*
         const int kstar = static_cast<int>(gk >> 1);
-        const int d2 = (gk & 1u) ? -2 : 2;         // 2 d, d = 1 - 2 x_k*
+        const int xk = static_cast<int>(gk & 1u);
+        const int C = xk ? -512 : 512;          // 512 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;
         const int8_t *qrow = Q8 + static_cast<int64_t>(kstar) * n_pad;
+        uint4 w[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const int j0 = c * CH + 4 * t;
-            if (j0 < n_pad) {
-                const char4 q = *reinterpret_cast<const char4 *>(qrow + j0);
-                const int qq[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int xb = (xm >> (4 * c + e)) & 1;
-                    const int coef = xb ? -d2 : d2;  // 2 d (1 - 2 x_j)
-                    if (j0 + e == kstar) {
-                        D[c][e] = -D[c][e];
-                        xm ^= 1u << (4 * c + e);
-                    } else {
-                        D[c][e] += coef * qq[e];
-                    }
-                }
+            const int j0 = c * A::CHUNK + 16 * t;
+            w[c] = j0 < n_pad ? __ldg(reinterpret_cast<const uint4 *>(qrow + j0)) : make_uint4(0, 0, 0, 0);
+        }
+        if (((kstar % A::CHUNK) >> 4) == t) {
+            const int li = (kstar / A::CHUNK) * 16 + (kstar & 15);
+            const int x_new = xk ^ 1;
+            switch (li) {
+                UBQP_CASE8(0) UBQP_CASE8(8) UBQP_CASE8(16) UBQP_CASE8(24)
+                UBQP_CASE8(32) UBQP_CASE8(40) UBQP_CASE8(48) UBQP_CASE8(56)
+                UBQP_CASE8(64) UBQP_CASE8(72) UBQP_CASE8(80) UBQP_CASE8(88)
+                UBQP_CASE8(96) UBQP_CASE8(104) UBQP_CASE8(112) UBQP_CASE8(120)
+                default: break;
             }
         }
+        // ---- fused update + next argmax
+        int r0 = kPad, r1 = kPad, r2 = kPad, r3 = kPad;
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+#pragma unroll
+            for (int wi = 0; wi < 4; ++wi) {
+                const uint32_t sq = neg_bytes(word_of(w[c], wi), m[c][wi]);
+                int &k0 = K[c][4 * wi + 0];
+                int &k1 = K[c][4 * wi + 1];
+                int &k2 = K[c][4 * wi + 2];
+                int &k3 = K[c][4 * wi + 3];
+                k0 += sext_byte(sq, sel_of(0)) * C;
+                k1 += sext_byte(sq, sel_of(1)) * C;
+                k2 += sext_byte(sq, sel_of(2)) * C;
+                k3 += sext_byte(sq, sel_of(3)) * C;
+                r0 = max(r0, k0);
+                r1 = max(r1, k1);
+                r2 = max(r2, k2);
+                r3 = max(r3, k3);
+            }
+        }
+        run = max(max(r0, r1), max(r2, r3));
     }
 
     // ---- outputs
     if (bits_out) {
-        for (int w = t; w < (CH * NCH) / 32; w += BLOCK) s_bits[w] = 0;
+        for (int w2 = t; w2 < (A::CHUNK * NCH) / 32; w2 += BLOCK) s_bits[w2] = 0;
         __syncthreads();
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
-            const int j0 = c * CH + 4 * t;
-            const uint32_t b4 = (xm >> (4 * c)) & 15u;
-            if (b4) atomicOr(&s_bits[j0 >> 5], b4 << (j0 & 31));
+            const int j0 = c * A::CHUNK + 16 * t;
+            uint32_t b16 = 0;
+#pragma unroll
+            for (int wi = 0; wi < 4; ++wi) b16 |= nibble_of_byte_mask(m[c][wi]) << (4 * wi);
+            if (b16) atomicOr(&s_bits[j0 >> 5], b16 << (j0 & 31));
         }
         __syncthreads();
-        for (int w = t; w < W64; w += BLOCK)
-            bits_out[static_cast<int64_t>(i) * W64 + w] =
-                static_cast<uint64_t>(s_bits[2 * w]) | (static_cast<uint64_t>(s_bits[2 * w + 1]) << 32);
+        for (int w2 = t; w2 < W64; w2 += BLOCK)
+            bits_out[static_cast<int64_t>(i) * W64 + w2] =
+                static_cast<uint64_t>(s_bits[2 * w2]) | (static_cast<uint64_t>(s_bits[2 * w2 + 1]) << 32);
     }
     if (t == 0) {
         if (f_out) f_out[i] = fv;
@@ -153,13 +250,17 @@ ascend_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n
         }
     }
 }
+#undef UBQP_CASE8
+#undef UBQP_CASE
 
 template <int BLOCK, int NCH>
 void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_dev,
                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
-    ascend_kernel<BLOCK, NCH><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
-        slots, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
-        c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
+    // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
+    constexpr int kMinBlocks = BLOCK == 32 ? 12 : (BLOCK == 64 ? 6 : (BLOCK == 128 ? 4 : 2));
+    ascend_kernel<BLOCK, NCH, kMinBlocks><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
+        slots, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f, c.Xb,
+        f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
 }
 
 }  // namespace
@@ -169,24 +270,26 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
                   int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     if (m <= 0) return 0;
     const int np = c.n_pad;
-#define UBQP_ASC(B, N)                                                                 \
-    do {                                                                               \
+#define UBQP_ASC(B, N)                                                                      \
+    do {                                                                                    \
         launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev); \
-        ++c.launches;                                                                  \
-        return 0;                                                                      \
+        ++c.launches;                                                                       \
+        return 0;                                                                           \
     } while (0)
-    if (np <= 1024) UBQP_ASC(256, 1);
-    if (np <= 2048) UBQP_ASC(256, 2);
-    if (np <= 3072) UBQP_ASC(256, 3);
-    if (np <= 4096) UBQP_ASC(256, 4);
-    if (np <= 5120) UBQP_ASC(256, 5);
-    if (np <= 6144) UBQP_ASC(256, 6);
-    if (np <= 7168) UBQP_ASC(256, 7);
-    if (np <= 8192) UBQP_ASC(256, 8);
-    if (np <= 10240) UBQP_ASC(512, 5);
-    if (np <= 12288) UBQP_ASC(512, 6);
-    if (np <= 14336) UBQP_ASC(512, 7);
-    if (np <= 16384) UBQP_ASC(512, 8);
+    // smallest CTA with <= 5 sixteen-variable chunks per thread (<= 80 register keys)
+    if (np <= 512) UBQP_ASC(32, 1);
+    if (np <= 1024) UBQP_ASC(32, 2);
+    if (np <= 1536) UBQP_ASC(32, 3);
+    if (np <= 2048) UBQP_ASC(32, 4);
+    if (np <= 2560) UBQP_ASC(32, 5);
+    if (np <= 3072) UBQP_ASC(64, 3);
+    if (np <= 4096) UBQP_ASC(64, 4);
+    if (np <= 5120) UBQP_ASC(64, 5);
+    if (np <= 6144) UBQP_ASC(128, 3);
+    if (np <= 8192) UBQP_ASC(128, 4);
+    if (np <= 10240) UBQP_ASC(128, 5);
+    if (np <= 12288) UBQP_ASC(256, 3);
+    if (np <= 16384) UBQP_ASC(256, 4);
 #undef UBQP_ASC
     return 1;
 }

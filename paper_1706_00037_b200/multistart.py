@@ -96,7 +96,9 @@ class MultiStart:
         self.k_local = len(range(self.rank, self.K, self.world))
         self.lam = float(lam)
         self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
-        self.stream = torch.cuda.current_stream(self.device)
+        # one non-default stream shared by torch (collectives, small ops) and libubqp.so
+        self.stream = torch.cuda.Stream(device=self.device)
+        torch.cuda.set_stream(self.stream)
         self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
         self.u.load_Q(np.ascontiguousarray(Q, dtype=np.int32), max(self.k_local, 1))
         self.W64 = self.u.W64
