@@ -12,11 +12,12 @@
 // Q8 (= column k*, Q symmetric; n bytes) with one 16-byte load per chunk.  Each gain is
 // held in a register as a totally ordered key
 //     K_j = 256 Delta_j + 2 (127 - li) + x_j          (li = 16c + e, the local index)
-// so the running argmax (largest Delta, then lowest j) is one IMNMX per element and the
-// update is one IMAD with a block-uniform multiplier C = 512 d applied to the byte
-// s_j Q_{k* j}; the per-variable sign s_j = 1 - 2 x_j is applied to 4 packed bytes at once
-// (x is held as byte masks).  Per element and step: PRMT + IMAD + IMNMX + 1/4 of the
-// packed sign fix-up.  The owner of k* pre-compensates K_k* through a jump table so the
+// so the running argmax (largest Delta, then lowest j) is a 3-input IMNMX per two
+// elements, and the update K_j += C s_j Q_{k* j} (C = 512 d, block-uniform) is one IDP.2A
+// per element on FMA pipe: x is held as byte masks m (0xFF where x = 1), t = q ^ m is the
+// ones' complement of the negated bytes, and the (t_e, m_e) byte pairs dotted with
+// (C, -C) give C (t_e - m_e) = C s_e q_e exactly.  Per 4 elements and step: 1 LOP3 +
+// 2 PRMT + 2 IMNMX3 (ALU pipe) and 4 IDP.2A (FMA pipe).  The owner of k* pre-compensates K_k* through a jump table so the
 // fused loop needs no per-element test.  Argmax across lanes: __reduce_max/min_sync;
 // across warps: one __syncthreads over double-buffered shared slots.
 #include <climits>
@@ -37,10 +38,16 @@ __device__ __forceinline__ int sext_byte(uint32_t w, uint32_t sel) {
 __device__ __forceinline__ constexpr uint32_t sel_of(int b) {
     return static_cast<uint32_t>(b) | ((8u | b) << 4) | ((8u | b) << 8) | ((8u | b) << 12);
 }
-// negate the bytes of w selected by mask m (0xFF per negated byte), no carries across bytes
-__device__ __forceinline__ uint32_t neg_bytes(uint32_t w, uint32_t m) {
-    const uint32_t t = w ^ m;
-    return ((t & 0x7F7F7F7Fu) + (m & 0x01010101u)) ^ (t & 0x80808080u);
+// c + a.s16[0] * b.s8[0|2] + a.s16[1] * b.s8[1|3]  (IDP.2A)
+__device__ __forceinline__ int dp2a_lo(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+__device__ __forceinline__ int dp2a_hi(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
 }
 __device__ __forceinline__ uint32_t byte_mask_of_nibble(uint32_t nib) {
     return ((nib * 0x00204081u) & 0x01010101u) * 0xFFu;
@@ -197,28 +204,32 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
                 default: break;
             }
         }
-        // ---- fused update + next argmax
-        int r0 = kPad, r1 = kPad, r2 = kPad, r3 = kPad;
+        // ---- fused update + next argmax.  Per 4 variables: t = w ^ m gives ~q where x = 1;
+        // interleave (t_e, m_e) byte pairs and let IDP2A add C t_e - C m_e = C s_e q_e
+        // (m_e = -1 where x_e = 1, so the ones' complement is completed exactly).
+        const uint32_t a2 = (static_cast<uint32_t>(C) & 0xFFFFu) | (static_cast<uint32_t>(-C) << 16);
+        int r0 = kPad, r1 = kPad;
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
 #pragma unroll
             for (int wi = 0; wi < 4; ++wi) {
-                const uint32_t sq = neg_bytes(word_of(w[c], wi), m[c][wi]);
+                const uint32_t mw = m[c][wi];
+                const uint32_t tq = word_of(w[c], wi) ^ mw;
+                const uint32_t blo = __byte_perm(tq, mw, 0x5140);
+                const uint32_t bhi = __byte_perm(tq, mw, 0x7362);
                 int &k0 = K[c][4 * wi + 0];
                 int &k1 = K[c][4 * wi + 1];
                 int &k2 = K[c][4 * wi + 2];
                 int &k3 = K[c][4 * wi + 3];
-                k0 += sext_byte(sq, sel_of(0)) * C;
-                k1 += sext_byte(sq, sel_of(1)) * C;
-                k2 += sext_byte(sq, sel_of(2)) * C;
-                k3 += sext_byte(sq, sel_of(3)) * C;
-                r0 = max(r0, k0);
-                r1 = max(r1, k1);
-                r2 = max(r2, k2);
-                r3 = max(r3, k3);
+                k0 = dp2a_lo(a2, blo, k0);
+                k1 = dp2a_hi(a2, blo, k1);
+                k2 = dp2a_lo(a2, bhi, k2);
+                k3 = dp2a_hi(a2, bhi, k3);
+                r0 = max(r0, max(k0, k1));
+                r1 = max(r1, max(k2, k3));
             }
         }
-        run = max(max(r0, r1), max(r2, r3));
+        run = max(r0, r1);
     }
 
     // ---- outputs
