@@ -21,6 +21,8 @@
 // fused loop needs no per-element test.  Argmax across lanes: __reduce_max/min_sync;
 // across warps: one __syncthreads over double-buffered shared slots.
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ubqp_internal.cuh"
 
@@ -143,6 +145,10 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
 #pragma unroll
         for (int e = 0; e < 16; ++e) run = max(run, K[c][e]);
 
+    const int8_t *qbase = Q8 + 16 * t;        // + kstar*n_pad + c*CHUNK per step
+    bool cvalid[NCH];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) cvalid[c] = c * A::CHUNK + 16 * t < n_pad;
     int64_t fv = f_in[s];
     int flips = 0;
     int par = 0;
@@ -186,13 +192,11 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         const int C = xk ? -512 : 512;          // 512 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;
-        const int8_t *qrow = Q8 + static_cast<int64_t>(kstar) * n_pad;
+        const int8_t *qrow = qbase + static_cast<int64_t>(kstar) * n_pad;
         uint4 w[NCH];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int j0 = c * A::CHUNK + 16 * t;
-            w[c] = j0 < n_pad ? __ldg(reinterpret_cast<const uint4 *>(qrow + j0)) : make_uint4(0, 0, 0, 0);
-        }
+        for (int c = 0; c < NCH; ++c)
+            w[c] = cvalid[c] ? __ldg(reinterpret_cast<const uint4 *>(qrow + c * A::CHUNK)) : make_uint4(0, 0, 0, 0);
         if (((kstar % A::CHUNK) >> 4) == t) {
             const int li = (kstar / A::CHUNK) * 16 + (kstar & 15);
             const int x_new = xk ^ 1;
@@ -208,28 +212,33 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         // interleave (t_e, m_e) byte pairs and let IDP2A add C t_e - C m_e = C s_e q_e
         // (m_e = -1 where x_e = 1, so the ones' complement is completed exactly).
         const uint32_t a2 = (static_cast<uint32_t>(C) & 0xFFFFu) | (static_cast<uint32_t>(-C) << 16);
-        int r0 = kPad, r1 = kPad;
+        int r0 = kPad, r1 = kPad, r2 = kPad, r3 = kPad;   // 4 independent max chains
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
 #pragma unroll
             for (int wi = 0; wi < 4; ++wi) {
                 const uint32_t mw = m[c][wi];
                 const uint32_t tq = word_of(w[c], wi) ^ mw;
-                const uint32_t blo = __byte_perm(tq, mw, 0x5140);
-                const uint32_t bhi = __byte_perm(tq, mw, 0x7362);
                 int &k0 = K[c][4 * wi + 0];
                 int &k1 = K[c][4 * wi + 1];
                 int &k2 = K[c][4 * wi + 2];
                 int &k3 = K[c][4 * wi + 3];
+                const uint32_t blo = __byte_perm(tq, mw, 0x5140);   // t0 m0 t1 m1
+                const uint32_t bhi = __byte_perm(tq, mw, 0x7362);   // t2 m2 t3 m3
                 k0 = dp2a_lo(a2, blo, k0);
                 k1 = dp2a_hi(a2, blo, k1);
                 k2 = dp2a_lo(a2, bhi, k2);
                 k3 = dp2a_hi(a2, bhi, k3);
-                r0 = max(r0, max(k0, k1));
-                r1 = max(r1, max(k2, k3));
+                if (wi & 1) {
+                    r2 = max(r2, max(k0, k1));
+                    r3 = max(r3, max(k2, k3));
+                } else {
+                    r0 = max(r0, max(k0, k1));
+                    r1 = max(r1, max(k2, k3));
+                }
             }
         }
-        run = max(r0, r1);
+        run = max(max(r0, r1), max(r2, r3));
     }
 
     // ---- outputs
@@ -268,7 +277,8 @@ template <int BLOCK, int NCH>
 void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_dev,
                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
-    constexpr int kMinBlocks = BLOCK == 32 ? 12 : (BLOCK == 64 ? 6 : (BLOCK == 128 ? 4 : 2));
+    // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
+    constexpr int kMinBlocks = (65536 / (BLOCK * (24 * NCH + 48))) < 1 ? 1 : 65536 / (BLOCK * (24 * NCH + 48));
     ascend_kernel<BLOCK, NCH, kMinBlocks><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
         slots, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f, c.Xb,
         f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
@@ -276,31 +286,31 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
 
 }  // namespace
 
-// returns 0 on success, 1 if n is outside the instantiated range
+// Shape: NCH = 5 sixteen-variable chunks per thread (80 register keys) and the smallest
+// multiple of 32 threads covering n_pad; below 2560 variables one warp with fewer chunks.
+// UBQP_ASC_CFG="BLOCK,NCH" forces a shape (tuning sweeps, tools/asc_sweep.py).
+// Returns 0 on success, 1 if n is outside the instantiated range.
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                   int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     if (m <= 0) return 0;
     const int np = c.n_pad;
-#define UBQP_ASC(B, N)                                                                      \
-    do {                                                                                    \
-        launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev); \
-        ++c.launches;                                                                       \
-        return 0;                                                                           \
-    } while (0)
-    // smallest CTA with <= 5 sixteen-variable chunks per thread (<= 80 register keys)
-    if (np <= 512) UBQP_ASC(32, 1);
-    if (np <= 1024) UBQP_ASC(32, 2);
-    if (np <= 1536) UBQP_ASC(32, 3);
-    if (np <= 2048) UBQP_ASC(32, 4);
-    if (np <= 2560) UBQP_ASC(32, 5);
-    if (np <= 3072) UBQP_ASC(64, 3);
-    if (np <= 4096) UBQP_ASC(64, 4);
-    if (np <= 5120) UBQP_ASC(64, 5);
-    if (np <= 6144) UBQP_ASC(128, 3);
-    if (np <= 8192) UBQP_ASC(128, 4);
-    if (np <= 10240) UBQP_ASC(128, 5);
-    if (np <= 12288) UBQP_ASC(256, 3);
-    if (np <= 16384) UBQP_ASC(256, 4);
+    int fb = 0, fn = 0;
+    if (const char *env = getenv("UBQP_ASC_CFG")) {
+        if (sscanf(env, "%d,%d", &fb, &fn) != 2 || fb * 16 * fn < np) fb = fn = 0;
+    }
+    if (!fb) {
+        if (np <= 2560) { fb = 32; fn = (np + 511) / 512; }
+        else { fb = 32 * ((np + 32 * 80 - 1) / (32 * 80)); fn = 5; }
+    }
+#define UBQP_ASC(B, N)                                                                          \
+    if (fb == B && fn == N) {                                                                   \
+        launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);    \
+        ++c.launches;                                                                           \
+        return 0;                                                                               \
+    }
+    UBQP_ASC(32, 1) UBQP_ASC(32, 2) UBQP_ASC(32, 3) UBQP_ASC(32, 4) UBQP_ASC(32, 5)
+    UBQP_ASC(64, 4) UBQP_ASC(64, 5) UBQP_ASC(96, 4) UBQP_ASC(96, 5) UBQP_ASC(128, 4) UBQP_ASC(128, 5)
+    UBQP_ASC(160, 5) UBQP_ASC(192, 5) UBQP_ASC(224, 5)
 #undef UBQP_ASC
     return 1;
 }

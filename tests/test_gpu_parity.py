@@ -256,3 +256,41 @@ def test_full_size_sampled(n, K, kind):
     idx = np.unique(np.concatenate([[0, 1, K - 1], rng.integers(0, K, 61)]))
     assert np.array_equal(f[idx], oracle.eval_batch(Q, Xs(idx), nthreads=8))
     assert st.sum == int(f.sum()) and st.count == K
+
+
+@pytest.mark.parametrize("n", [5000, 7000])
+def test_ascend_full_size(n):
+    """The bench shapes (64x5 at n = 5000, 96x5 at n = 7000), exact against the oracle."""
+    Q = generate_Q(n, 1.0, seed=4)
+    K = 24
+    u = _handle_with(Q, K)
+    b = np.zeros(u.W64, np.uint64)
+    u.first_derivative(b)
+    x0 = unpack_bits(b, n)[0]
+    u.diversify(b, 600, K)                     # Glover solutions near the first-derivative start
+    u.eval_batch(UBQP_EMIT_GAINS)
+    slots = np.arange(K, dtype=np.int32)
+    f_o = np.zeros(K, np.int64)
+    fl_o = np.zeros(K, np.int32)
+    b_o = np.zeros((K, u.W64), np.uint64)
+    u.ascend(slots, K, 10 * n, f_o, fl_o, b_o)
+    X0 = oracle.diversify(x0, 600, K)
+    Xr, fr, flr = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0, nthreads=8), 10 * n, nthreads=8)
+    assert np.array_equal(f_o, fr) and np.array_equal(fl_o, flr)
+    assert np.array_equal(unpack_bits(b_o, n), Xr)
+
+
+@pytest.mark.parametrize("shape", ["32,5", "64,4", "64,5", "96,4", "128,4", "160,5"])
+def test_ascend_forced_shapes(shape, monkeypatch):
+    n, K = 2500, 40
+    Q = generate_Q(n, 0.5, seed=8)
+    u = _handle_with(Q, K)
+    u.random(9, K)
+    u.eval_batch(UBQP_EMIT_GAINS)
+    monkeypatch.setenv("UBQP_ASC_CFG", shape)
+    f_o = np.zeros(K, np.int64)
+    b_o = np.zeros((K, u.W64), np.uint64)
+    u.ascend(np.arange(K, dtype=np.int32), K, 100000, f_o, None, b_o)
+    X0 = oracle.random_solutions(n, 9, K)
+    Xr, fr, _ = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0, nthreads=8), 100000, nthreads=8)
+    assert np.array_equal(f_o, fr) and np.array_equal(unpack_bits(b_o, n), Xr)
