@@ -154,12 +154,46 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
                 int64_t *f_out, int32_t *flips_out, uint64_t *bits_out,
                 int64_t *best_key_out);
 
+/* ---------------------------------------------------------------------------------
+ * Real-valued Q (a4': "Q ... of real or integer coefficients"; "float or double",
+ * P:89).  The coefficients are rounded once to 28-bit fixed point,
+ *     Q~ = 2^-e round(Q 2^e),   e = max{e : max|Q_ij| 2^e <= 2^27 - 1},
+ * and Q~ 2^e is stored as 4 int8 planes of balanced base-128 digits (|digit| <= 64), so each
+ * plane runs through the same exact int8 tensor-core evaluation; f = 2^-e sum_s 128^s x^t L_s x
+ * is the exact objective of Q~ (one final rounding to binary64).  Error bound:
+ * |f - x^t Q x| <= |x|^2 2^-(e+1) (+ one binary64 rounding).  The ascent stays integer-only.
+ * ------------------------------------------------------------------------------ */
+enum { UBQP_F32 = 1, UBQP_F64 = 2 };
+
+/* integer image statistics of a real-Q batch: f~_k = f_k 2^e (exact int64):
+ * sum f~ as a two's-complement int128 (sum_hi:sum_lo), count, max f~ (INT64_MIN if empty). */
+typedef struct {
+    int64_t sum_hi;
+    int64_t sum_lo;
+    int64_t count;
+    int64_t max_fint;
+} ubqp_stats_real;
+
+/* Load a real-valued symmetric Q (row-major n*n float32 or float64, host or device).
+ * Errors: E_NOT_SYMMETRIC, E_RANGE (non-finite), E_INVALID.  Replaces any earlier Q.
+ * Batch generation calls work unchanged; integer-only calls return E_STATE. */
+int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_max);
+
+/* Evaluate the batch against the real Q: f_out double[k_local] (may be NULL), stats_out
+ * (may be NULL).  4 int8 tensor-core passes + an exact integer combine. */
+int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out);
+
+/* Screen the last real batch: T = mean + lambda (max_value - mean) (binary64, no
+ * contraction); survivors {k : f_k > T} ascending.  Synchronises. */
+int ubqp_screen_real(ubqp_t h, double lambda, double mean, double max_value, int32_t *surv_out,
+                     int64_t *m_out, double *T_out);
+
 /* Wait for all work queued on the handle's stream. */
 int ubqp_sync(ubqp_t h);
 
 /* Introspection (read-only): n, n_pad, W64, k_max, k_local, kernels launched so far. */
 enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
-       UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6 };
+       UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8 };
 int ubqp_query(ubqp_t h, int what, int64_t *value);
 
 #ifdef __cplusplus

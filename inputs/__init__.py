@@ -8,7 +8,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["generate_Q", "pack_bits", "unpack_bits", "CONFIGS"]
+__all__ = ["generate_Q", "generate_Q_real", "pack_bits", "unpack_bits", "CONFIGS"]
 
 
 def generate_Q(n: int, density: float, low: int = -100, high: int = 100, seed: int = 0) -> np.ndarray:
@@ -29,6 +29,20 @@ def generate_Q(n: int, density: float, low: int = -100, high: int = 100, seed: i
     v = vals[rng.integers(0, vals.size, size=iu.shape[0])]
     v = np.where(keep, v, 0).astype(np.int32)
     Q = np.zeros((n, n), dtype=np.int32)
+    Q[iu, ju] = v
+    Q[ju, iu] = v
+    return Q
+
+
+def generate_Q_real(n: int, density: float, low: float = -100.0, high: float = 100.0, seed: int = 0,
+                    dtype=np.float64) -> np.ndarray:
+    """Symmetric real instance (SURVEY Appendix B setup): pairs i <= j nonzero w.p. density,
+    values uniform in [low, high)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    iu, ju = np.triu_indices(n)
+    keep = rng.random(iu.shape[0]) < density
+    v = np.where(keep, rng.uniform(low, high, size=iu.shape[0]), 0.0).astype(dtype)
+    Q = np.zeros((n, n), dtype=dtype)
     Q[iu, ju] = v
     Q[ju, iu] = v
     return Q

@@ -21,7 +21,7 @@ _lib = None
 __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "max_key", "stats", "threshold", "screen", "ascend",
-    "first_derivative_start", "run_rounds",
+    "first_derivative_start", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
 ]
 
 
@@ -224,3 +224,27 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
             inc_f, inc_x = best
             traj.append((rnd, inc_f))
     return inc_f, inc_x, traj
+
+
+# O9 -- real Q: f = sum of Q_ij over i, j with x_i = x_j = 1, correctly rounded ("real or
+# integer coefficients"; "float or double").  math.fsum is exactly rounded.
+def xQx_real(Q, x) -> float:
+    import math
+    Q = np.asarray(Q, dtype=np.float64)
+    x = np.asarray(x).reshape(-1).astype(bool)
+    S = np.flatnonzero(x)
+    return math.fsum(Q[np.ix_(S, S)].ravel().tolist())
+
+
+def eval_batch_real(Q, X) -> np.ndarray:
+    X = np.asarray(X)
+    if X.ndim == 1:
+        X = X.reshape(1, -1)
+    return np.array([xQx_real(Q, x) for x in X], dtype=np.float64)
+
+
+def first_derivative_start_real(Q) -> np.ndarray:
+    """x_i = 1 iff sum_j Q_ij > 0, row sums exactly rounded."""
+    import math
+    Q = np.asarray(Q, dtype=np.float64)
+    return np.array([1 if math.fsum(row.tolist()) > 0 else 0 for row in Q], dtype=np.uint8)

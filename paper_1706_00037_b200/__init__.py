@@ -3,6 +3,7 @@
 tcgen05 tensor cores -> T(lambda) screen -> batched steepest ascent, behind the C-ABI
 of include/ubqp.h (libubqp.so).  See DESIGN.md.
 """
-from .ubqp import EXPORTS, UBQP_EMIT_GAINS, Ubqp, UbqpError, load_library, ubqp_stats  # noqa: F401
+from .ubqp import (EXPORTS, UBQP_EMIT_GAINS, Ubqp, UbqpError, load_library, ubqp_stats,  # noqa: F401
+                   ubqp_stats_real)
 
-__all__ = ["Ubqp", "UbqpError", "load_library", "ubqp_stats", "UBQP_EMIT_GAINS", "EXPORTS"]
+__all__ = ["Ubqp", "UbqpError", "load_library", "ubqp_stats", "ubqp_stats_real", "UBQP_EMIT_GAINS", "EXPORTS"]

@@ -80,6 +80,11 @@ void free_batch(Ctx &c) {
 void free_all(Ctx &c) {
     free_batch(c);
     dfree(c.Q8); dfree(c.diag); dfree(c.seed); dfree(c.scratch64);
+    for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
+    dfree(c.fs); dfree(c.fint); dfree(c.freal);
+    c.real = false;
+    c.freal_valid = false;
+    c.q_exp = 0;
     c.n = 0;
 }
 
@@ -374,6 +379,7 @@ int ubqp_get_batch(ubqp_t h, uint64_t *bits_out) {
 
 int ubqp_eval_batch(ubqp_t h, int flags, int64_t *f_out, ubqp_stats *stats_out) {
     GUARD(h);
+    if (h->real) return fail(h, UBQP_E_STATE, "ubqp: real-valued Q loaded: use ubqp_eval_batch_real");
     if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch to evaluate");
     if (flags & ~UBQP_EMIT_GAINS) return fail(h, UBQP_E_INVALID, "ubqp: unknown flags");
     int rc = run_eval(h, (flags & UBQP_EMIT_GAINS) != 0);
@@ -413,6 +419,7 @@ int ubqp_get_gains(ubqp_t h, int64_t slot0, int64_t count, int32_t *gains_out) {
 int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count, int64_t max_value,
                 int32_t *surv_out, int64_t *m_out, double *T_out) {
     GUARD(h);
+    if (h->real) return fail(h, UBQP_E_STATE, "ubqp: real-valued Q loaded: use ubqp_screen_real");
     if (!std::isfinite(lambda)) return fail(h, UBQP_E_INVALID, "ubqp: lambda is not finite");
     if (mean_count <= 0) return fail(h, UBQP_E_STATE, "ubqp: mean_count <= 0");
     if (!h->f_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated batch");
@@ -451,6 +458,7 @@ int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count, i
 int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_out,
                 int32_t *flips_out, uint64_t *bits_out, int64_t *best_key_out) {
     GUARD(h);
+    if (h->real) return fail(h, UBQP_E_STATE, "ubqp: the ascent runs on integer Q only");
     if (!h->f_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated batch");
     if (m < 0 || m > h->k_local || max_flips < 0 || (!slots && m > 0))
         return fail(h, UBQP_E_INVALID, "ubqp: bad ascend arguments");
@@ -496,6 +504,158 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, in
     return UBQP_OK;
 }
 
+// ---------------------------------------------------------------- real-valued Q (a4')
+int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_max) {
+    GUARD(h);
+    if (!Q || n < 1 || n > 16384) return fail(h, UBQP_E_INVALID, "ubqp: n must be in [1, 16384]");
+    if (dtype != UBQP_F32 && dtype != UBQP_F64) return fail(h, UBQP_E_INVALID, "ubqp: dtype must be UBQP_F32 or UBQP_F64");
+    if (k_max < 1 || k_max > (1ll << 22)) return fail(h, UBQP_E_INVALID, "ubqp: k_max must be in [1, 2^22]");
+    const int64_t nn = static_cast<int64_t>(n) * n;
+    const size_t esz = dtype == UBQP_F32 ? 4 : 8;
+    std::vector<unsigned char> raw;
+    const void *Qh = Q;
+    if (is_device_ptr(Q)) {
+        raw.resize(nn * esz);
+        CK(cudaMemcpy(raw.data(), Q, nn * esz, cudaMemcpyDeviceToHost));
+        Qh = raw.data();
+    }
+    auto at = [&](int64_t idx) -> double {
+        return dtype == UBQP_F32 ? static_cast<double>(static_cast<const float *>(Qh)[idx])
+                                 : static_cast<const double *>(Qh)[idx];
+    };
+    double amax = 0.0;
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            const double v = at(static_cast<int64_t>(i) * n + j);
+            if (!std::isfinite(v)) return fail(h, UBQP_E_RANGE, "ubqp: non-finite coefficient");
+            if (j > i && v != at(static_cast<int64_t>(j) * n + i))
+                return fail(h, UBQP_E_NOT_SYMMETRIC, "ubqp: Q is not symmetric");
+            amax = std::fabs(v) > amax ? std::fabs(v) : amax;
+        }
+    // 28-bit fixed point: |round(Q 2^e)| <= 2^27 - 1 = the range of 4 balanced base-128 limbs
+    int e = 0;
+    if (amax > 0) {
+        e = static_cast<int>(std::floor(std::log2((134217727.0) / amax)));
+        while (e > -1000 && std::ldexp(amax, e) > 134217727.0) --e;
+        while (std::ldexp(amax, e + 1) <= 134217727.0 && e < 1000) ++e;
+    }
+    if (e < -900 || e > 900) return fail(h, UBQP_E_RANGE, "ubqp: coefficient scale out of range");
+    CK(cudaStreamSynchronize(h->stream));
+    free_all(*h);
+    CK(cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)));
+    h->n = n;
+    h->n_pad = (n + ubqp::kNPadAlign - 1) / ubqp::kNPadAlign * ubqp::kNPadAlign;
+    h->q_rows = (n + ubqp::kQRowAlign - 1) / ubqp::kQRowAlign * ubqp::kQRowAlign;
+    h->W64 = (n + 63) / 64;
+    h->real = true;
+    h->q_exp = e;
+    const size_t plane = static_cast<size_t>(h->q_rows) * h->n_pad;
+    std::vector<int8_t> L(plane * ubqp::kSlices, 0);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            long long v = std::llrint(std::ldexp(at(static_cast<int64_t>(i) * n + j), e));
+            for (int sl = 0; sl < ubqp::kSlices; ++sl) {
+                const long long r = ((v % 128) + 128) % 128;
+                const long long d = r >= 64 ? r - 128 : r;         // balanced digit in [-64, 63]
+                L[sl * plane + static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(d);
+                v = (v - d) / 128;
+            }
+        }
+    const int64_t nblk = (k_max + 4095) / 4096 + 1;
+    h->k_max = k_max;
+    h->k_cap_pad = (k_max + ubqp::kBM - 1) / ubqp::kBM * ubqp::kBM;
+    bool ok = cudaMalloc(&h->seed, h->W64 * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&h->diag, h->q_rows * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&h->Xb, k_max * h->W64 * sizeof(uint64_t)) == cudaSuccess &&
+              cudaMalloc(&h->X8, h->k_cap_pad * h->n_pad) == cudaSuccess &&
+              cudaMalloc(&h->f, k_max * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&h->fs, ubqp::kSlices * k_max * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&h->fint, k_max * sizeof(int64_t)) == cudaSuccess &&
+              cudaMalloc(&h->freal, k_max * sizeof(double)) == cudaSuccess &&
+              cudaMalloc(&h->surv, k_max * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&h->blk_count, nblk * sizeof(int32_t)) == cudaSuccess;
+    for (int sl = 0; ok && sl < ubqp::kSlices; ++sl) ok = cudaMalloc(&h->Qs[sl], plane) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        free_all(*h);
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the real-Q workspace");
+    }
+    CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));
+    for (int sl = 0; sl < ubqp::kSlices; ++sl) {
+        CK(cudaMemcpy(h->Qs[sl], L.data() + sl * plane, plane, cudaMemcpyHostToDevice));
+        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN)) {
+            free_all(*h);
+            return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
+        }
+    }
+    CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
+    if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM)) {
+        free_all(*h);
+        return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
+    }
+    h->k_local = -1;
+    CK(cudaDeviceSynchronize());
+    return UBQP_OK;
+}
+
+int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out) {
+    GUARD(h);
+    if (!h->real) return fail(h, UBQP_E_STATE, "ubqp: no real-valued Q loaded");
+    if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch to evaluate");
+    const int64_t k = h->k_local;
+    if (k > 0) {
+        CK(cudaMemsetAsync(h->fs, 0, ubqp::kSlices * h->k_max * sizeof(int64_t), h->stream));
+        for (int sl = 0; sl < ubqp::kSlices; ++sl) {
+            ubqp::launch_eval_tc(*h, k, false, &h->tmap_Qs[sl], h->fs + sl * h->k_max);
+            CK_LAUNCH("eval_tc_kernel (plane)");
+        }
+    }
+    ubqp::launch_combine_real(*h, k, h->scratch64 + 8);
+    CK_LAUNCH("combine_real_kernel");
+    h->freal_valid = true;
+    bool sync = false;
+    if (f_out && k > 0) {
+        const bool dev = is_device_ptr(f_out);
+        CK(cudaMemcpyAsync(f_out, h->freal, k * sizeof(double), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           h->stream));
+        sync |= !dev;
+    }
+    if (stats_out) {
+        const bool dev = is_device_ptr(stats_out);
+        CK(cudaMemcpyAsync(stats_out, h->scratch64 + 8, 4 * sizeof(int64_t),
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+        sync |= !dev;
+    }
+    if (sync) CK(cudaStreamSynchronize(h->stream));
+    return UBQP_OK;
+}
+
+int ubqp_screen_real(ubqp_t h, double lambda, double mean, double max_value, int32_t *surv_out,
+                     int64_t *m_out, double *T_out) {
+    GUARD(h);
+    if (!h->real || !h->freal_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated real-Q batch");
+    if (!std::isfinite(lambda) || !std::isfinite(mean) || !std::isfinite(max_value))
+        return fail(h, UBQP_E_INVALID, "ubqp: non-finite screen argument");
+    if (!m_out || (!surv_out && h->k_local > 0)) return fail(h, UBQP_E_INVALID, "ubqp: null output");
+    volatile double diff = max_value - mean;
+    volatile double scaled = lambda * diff;
+    const double T = mean + scaled;
+    if (T_out) *T_out = T;
+    ubqp::launch_screen_real(*h, h->k_local, T, h->scratch64 + 4);
+    CK_LAUNCH("screen kernels (real)");
+    int64_t m = 0;
+    CK(cudaMemcpyAsync(&m, h->scratch64 + 4, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (m > 0) {
+        const bool dev = is_device_ptr(surv_out);
+        CK(cudaMemcpyAsync(surv_out, h->surv, m * sizeof(int32_t), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           h->stream));
+        if (!dev) CK(cudaStreamSynchronize(h->stream));
+    }
+    *m_out = m;
+    return UBQP_OK;
+}
+
 int ubqp_sync(ubqp_t h) {
     GUARD(h);
     CK(cudaStreamSynchronize(h->stream));
@@ -512,6 +672,8 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
         case UBQP_Q_KLOCAL: *value = h->k_local; break;
         case UBQP_Q_LAUNCHES: *value = h->launches; break;
         case UBQP_Q_STREAM: *value = reinterpret_cast<int64_t>(h->stream); break;
+        case UBQP_Q_REAL_EXP: *value = h->real ? h->q_exp : 0; break;
+        case UBQP_Q_IS_REAL: *value = h->real ? 1 : 0; break;
         default: return UBQP_E_INVALID;
     }
     return UBQP_OK;

@@ -278,7 +278,8 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
     // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
-    constexpr int kMinBlocks = (65536 / (BLOCK * (24 * NCH + 48))) < 1 ? 1 : 65536 / (BLOCK * (24 * NCH + 48));
+    constexpr int kRegs = NCH >= 6 ? 256 : 24 * NCH + 48;
+    constexpr int kMinBlocks = (65536 / (BLOCK * kRegs)) < 1 ? 1 : 65536 / (BLOCK * kRegs);
     ascend_kernel<BLOCK, NCH, kMinBlocks><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
         slots, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f, c.Xb,
         f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
@@ -286,8 +287,10 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
 
 }  // namespace
 
-// Shape: NCH = 5 sixteen-variable chunks per thread (80 register keys) and the smallest
-// multiple of 32 threads covering n_pad; below 2560 variables one warp with fewer chunks.
+// Shape: NCH = 7 sixteen-variable chunks per thread (112 register keys) and the smallest
+// multiple of 32 threads covering n_pad (64 threads at n = 7000: 98% of the lanes carry a
+// variable); below 3584 variables one warp with fewer chunks.  Fewer, fuller threads
+// amortise the per-step argmax exchange (measured: 96x5 306 ms, 64x7 277 ms at config 4).
 // UBQP_ASC_CFG="BLOCK,NCH" forces a shape (tuning sweeps, tools/asc_sweep.py).
 // Returns 0 on success, 1 if n is outside the instantiated range.
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
@@ -298,19 +301,25 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
     if (const char *env = getenv("UBQP_ASC_CFG")) {
         if (sscanf(env, "%d,%d", &fb, &fn) != 2 || fb * 16 * fn < np) fb = fn = 0;
     }
-    if (!fb) {
-        if (np <= 2560) { fb = 32; fn = (np + 511) / 512; }
-        else { fb = 32 * ((np + 32 * 80 - 1) / (32 * 80)); fn = 5; }
-    }
+    int db, dn;   // default shape
+    if (np <= 3584) { db = 32; dn = (np + 511) / 512; }
+    else { db = 32 * ((np + 32 * 112 - 1) / (32 * 112)); dn = 7; }
+    if (!fb) { fb = db; fn = dn; }
 #define UBQP_ASC(B, N)                                                                          \
     if (fb == B && fn == N) {                                                                   \
         launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);    \
         ++c.launches;                                                                           \
         return 0;                                                                               \
     }
-    UBQP_ASC(32, 1) UBQP_ASC(32, 2) UBQP_ASC(32, 3) UBQP_ASC(32, 4) UBQP_ASC(32, 5)
-    UBQP_ASC(64, 4) UBQP_ASC(64, 5) UBQP_ASC(96, 4) UBQP_ASC(96, 5) UBQP_ASC(128, 4) UBQP_ASC(128, 5)
-    UBQP_ASC(160, 5) UBQP_ASC(192, 5) UBQP_ASC(224, 5)
+#define UBQP_ASC_ALL                                                                                  \
+    UBQP_ASC(32, 1) UBQP_ASC(32, 2) UBQP_ASC(32, 3) UBQP_ASC(32, 4) UBQP_ASC(32, 5) UBQP_ASC(32, 6)   \
+    UBQP_ASC(32, 7) UBQP_ASC(64, 7) UBQP_ASC(96, 7) UBQP_ASC(128, 7) UBQP_ASC(160, 7)                 \
+    UBQP_ASC(64, 5) UBQP_ASC(96, 5) UBQP_ASC(128, 4) UBQP_ASC(128, 5)
+    UBQP_ASC_ALL
+    fb = db;                       // a forced shape that is not instantiated: use the default
+    fn = dn;
+    UBQP_ASC_ALL
+#undef UBQP_ASC_ALL
 #undef UBQP_ASC
     return 1;
 }

@@ -13,6 +13,8 @@
 //   warps 2..5  : epilogue (tcgen05.ld 32x32b -> f partial / gains), TMEM double-buffered
 // Tiles are ordered n-fastest so the ~5 X bands in flight are shared through L2 by all
 // N tiles and Q (49 MB at n = 7000) stays L2-resident.
+#include <climits>
+
 #include "ubqp_internal.cuh"
 
 namespace ubqp {
@@ -155,7 +157,7 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
                             const int y2 = 2 * static_cast<int32_t>(v[i]);
                             o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
                         }
-                        gp[i4] = make_int4(o[0], o[1], o[2], o[3]);
+                        __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));   // streaming: keep X/Q in L2
                     }
                 }
             }
@@ -217,7 +219,7 @@ bool g_attr_set = false;
 
 }  // namespace
 
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains) {
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q, int64_t *f_out) {
     if (k <= 0) return;
     if (!g_attr_set) {
         cudaFuncSetAttribute(eval_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -230,8 +232,69 @@ void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains) {
     const int64_t num_tiles = num_m_tiles * num_n_tiles;
     const int grid = static_cast<int>(num_tiles < c.num_sms ? num_tiles : c.num_sms);
     eval_tc_kernel<<<grid, kThreads, kSmemBytes, c.stream>>>(
-        c.tmap_X8, c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb,
-        c.diag, c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+        c.tmap_X8, tmap_q ? *tmap_q : c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks,
+        num_tiles, c.Xb, c.diag, f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+    ++c.launches;
+}
+
+// ---------------------------------------------------------------- real-valued Q (a4')
+// f~_k = sum_s 128^s f_s,k (exact int64), f_k = 2^-q_exp f~_k; stats over the integer image:
+// {sum f~ as int128 (hi, lo), count, max f~} so ranks can reduce them exactly.
+__global__ void __launch_bounds__(1024) combine_real_kernel(const int64_t *__restrict__ fs, int64_t k_max,
+                                                            int64_t K, int q_exp,
+                                                            int64_t *__restrict__ fint,
+                                                            double *__restrict__ freal,
+                                                            int64_t *__restrict__ out) {
+    __shared__ unsigned long long s_lo[32];
+    __shared__ long long s_hi[32];
+    __shared__ long long s_max[32];
+    __int128 sum = 0;
+    long long mx = LLONG_MIN;
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+        int64_t v = 0;
+#pragma unroll
+        for (int s = kSlices - 1; s >= 0; --s) v = v * 128 + fs[s * k_max + i];
+        fint[i] = v;
+        freal[i] = ldexp(static_cast<double>(v), -q_exp);
+        sum += v;
+        mx = v > mx ? v : mx;
+    }
+    // reduce the int128 sum as (hi, lo) halves with carries
+    unsigned long long lo = static_cast<unsigned long long>(sum);
+    long long hi = static_cast<long long>(sum >> 64);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
+        const long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+        const unsigned long long nlo = lo + olo;
+        hi = hi + ohi + (nlo < lo ? 1 : 0);
+        lo = nlo;
+        const long long omx = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = omx > mx ? omx : mx;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+        s_max[threadIdx.x >> 5] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long L = 0;
+        long long H = 0, M = LLONG_MIN;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
+            const unsigned long long nl = L + s_lo[w];
+            H = H + s_hi[w] + (nl < L ? 1 : 0);
+            L = nl;
+            M = s_max[w] > M ? s_max[w] : M;
+        }
+        out[0] = H;
+        out[1] = static_cast<int64_t>(L);
+        out[2] = K;
+        out[3] = M;
+    }
+}
+
+void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev) {
+    combine_real_kernel<<<1, 1024, 0, c.stream>>>(c.fs, c.k_max, k, c.q_exp, c.fint, c.freal, stats_dev);
     ++c.launches;
 }
 

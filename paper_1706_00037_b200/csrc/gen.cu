@@ -115,9 +115,14 @@ __global__ void __launch_bounds__(256) expand_kernel(int64_t k, int n, int W64, 
     store_expanded(X8 + slot * n_pad + 64ll * w, word);
 }
 
-// x_i = [sum_j Q_ij > 0].  One warp per row i of Q8 (row sums fit int32: n*127).
-__global__ void __launch_bounds__(256) first_derivative_kernel(const int8_t *__restrict__ Q8, int n,
-                                                               int n_pad, int W64,
+// x_i = [sum_j Q_ij > 0].  One warp per 32 rows (per-plane row sums fit int32: n*127).
+// Real Q: the row sums of the integer image, sum_s 128^s (row sum of plane s), exact in int64.
+struct Planes {
+    const int8_t *p[kSlices];
+    int count;
+};
+
+__global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, int n, int n_pad, int W64,
                                                                uint32_t *__restrict__ bits32) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -126,11 +131,15 @@ __global__ void __launch_bounds__(256) first_derivative_kernel(const int8_t *__r
     uint32_t word = 0;
     for (int r = 0; r < 32; ++r) {
         const int i = warp * 32 + r;
-        int s = 0;
-        if (i < n)
-            for (int j = lane; j < n_pad; j += 32) s += Q8[static_cast<int64_t>(i) * n_pad + j];
-        s = __reduce_add_sync(0xffffffffu, s);
-        if (i < n && s > 0) word |= 1u << r;
+        long long tot = 0;
+        for (int pl = planes.count - 1; pl >= 0; --pl) {
+            int s = 0;
+            if (i < n)
+                for (int j = lane; j < n_pad; j += 32) s += planes.p[pl][static_cast<int64_t>(i) * n_pad + j];
+            s = __reduce_add_sync(0xffffffffu, s);
+            tot = tot * 128 + s;
+        }
+        if (i < n && tot > 0) word |= 1u << r;
     }
     if (lane == 0) bits32[warp] = word;
 }
@@ -164,8 +173,16 @@ void launch_expand(Ctx &c, int64_t k) {
 
 void launch_first_derivative(Ctx &c, uint64_t *bits_dev) {
     const int warps = 2 * c.W64;   // one warp per 32-bit output word
+    Planes pl{};
+    if (c.real) {
+        for (int s = 0; s < kSlices; ++s) pl.p[s] = c.Qs[s];
+        pl.count = kSlices;
+    } else {
+        pl.p[0] = c.Q8;
+        pl.count = 1;
+    }
     first_derivative_kernel<<<(warps * 32 + 255) / 256, 256, 0, c.stream>>>(
-        c.Q8, c.n, c.n_pad, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
+        pl, c.n, c.n_pad, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
     ++c.launches;
 }
 

@@ -12,8 +12,9 @@ constexpr int kScrThreads = 1024;
 constexpr int kScrPer = 4;                        // consecutive elements per thread
 constexpr int kScrChunk = kScrThreads * kScrPer;  // elements per block
 
-__global__ void __launch_bounds__(kScrThreads) screen_count(const int64_t *__restrict__ f, int64_t K,
-                                                            int64_t t, int32_t *__restrict__ cnt) {
+template <typename V>
+__global__ void __launch_bounds__(kScrThreads) screen_count(const V *__restrict__ f, int64_t K,
+                                                            V t, int32_t *__restrict__ cnt) {
     __shared__ int s[kScrThreads / 32];
     const int64_t base = static_cast<int64_t>(blockIdx.x) * kScrChunk + threadIdx.x * kScrPer;
     int c = 0;
@@ -29,8 +30,9 @@ __global__ void __launch_bounds__(kScrThreads) screen_count(const int64_t *__res
     }
 }
 
-__global__ void __launch_bounds__(kScrThreads) screen_write(const int64_t *__restrict__ f, int64_t K,
-                                                            int64_t t,
+template <typename V>
+__global__ void __launch_bounds__(kScrThreads) screen_write(const V *__restrict__ f, int64_t K,
+                                                            V t,
                                                             const int32_t *__restrict__ cnt,
                                                             int32_t *__restrict__ surv,
                                                             int64_t *__restrict__ m_out) {
@@ -76,8 +78,20 @@ void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev) {
         return;
     }
     const unsigned blocks = static_cast<unsigned>((k + kScrChunk - 1) / kScrChunk);
-    screen_count<<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count);
-    screen_write<<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count, c.surv, m_dev);
+    screen_count<int64_t><<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count);
+    screen_write<int64_t><<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count, c.surv, m_dev);
+    c.launches += 2;
+}
+
+// real-valued f (a4'): survivors f_k > T compared in binary64
+void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev) {
+    if (k <= 0) {
+        cudaMemsetAsync(m_dev, 0, sizeof(int64_t), c.stream);
+        return;
+    }
+    const unsigned blocks = static_cast<unsigned>((k + kScrChunk - 1) / kScrChunk);
+    screen_count<double><<<blocks, kScrThreads, 0, c.stream>>>(c.freal, k, T, c.blk_count);
+    screen_write<double><<<blocks, kScrThreads, 0, c.stream>>>(c.freal, k, T, c.blk_count, c.surv, m_dev);
     c.launches += 2;
 }
 

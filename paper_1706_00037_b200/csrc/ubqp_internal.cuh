@@ -20,6 +20,7 @@ constexpr int kUmmaK = 32;        // K per tcgen05.mma kind::i8
 constexpr int kStages = 4;        // smem pipeline depth
 constexpr int kNPadAlign = 128;   // n_pad multiple (K dim of the GEMM)
 constexpr int kQRowAlign = kBN;   // Q8 rows padded to a multiple of the N tile
+constexpr int kSlices = 4;        // int8 limb planes of a real-valued Q (28-bit fixed point)
 
 struct Ctx {
     int device = 0;
@@ -50,6 +51,15 @@ struct Ctx {
     int32_t *asc_slots = nullptr; int64_t asc_cap = 0;
     // TMA descriptors (64 B each, passed by value as __grid_constant__)
     CUtensorMap tmap_X8{}, tmap_Q8{};
+    // real-valued Q (a4'): Q~ = 2^-q_exp * sum_s 128^s L_s, int8 limb planes L_s in [-64, 63]
+    bool real = false;
+    int q_exp = 0;
+    int8_t *Qs[kSlices] = {nullptr, nullptr, nullptr, nullptr};
+    CUtensorMap tmap_Qs[kSlices]{};
+    int64_t *fs = nullptr;       // [kSlices][k_max] per-plane x^t L_s x
+    int64_t *fint = nullptr;     // [k_max] integer image f~ = sum_s 128^s f_s
+    double *freal = nullptr;     // [k_max] f = 2^-q_exp f~
+    bool freal_valid = false;
     int64_t launches = 0;
 };
 
@@ -58,12 +68,15 @@ struct Ctx {
 void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k);
 void launch_random(Ctx &c, uint64_t seed, int64_t k);
 void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
-void launch_first_derivative(Ctx &c, uint64_t *bits_dev);
+void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer or real planes
 // eval_tc.cu
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains);
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q = nullptr,
+                    int64_t *f_out = nullptr);
 void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev);
+void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
 // screen.cu
 void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);
+void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
 // ascend.cu
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,
                   int64_t *f_dev, int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);

@@ -23,13 +23,26 @@ Q_N, Q_NPAD, Q_W64, Q_KMAX, Q_KLOCAL, Q_LAUNCHES, Q_STREAM = range(7)
 # every entry point declared in include/ubqp.h
 EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ubqp_load_Q",
            "ubqp_diversify", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
-           "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_sync", "ubqp_query"]
+           "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_sync", "ubqp_query",
+           "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real"]
+UBQP_F32, UBQP_F64 = 1, 2
+Q_REAL_EXP, Q_IS_REAL = 7, 8
 
 
 class UbqpError(RuntimeError):
     def __init__(self, code, msg):
         super().__init__(f"ubqp error {code}: {msg}")
         self.code = code
+
+
+class ubqp_stats_real(ctypes.Structure):
+    """integer-image statistics of a real-Q batch (include/ubqp.h)"""
+    _fields_ = [("sum_hi", ctypes.c_int64), ("sum_lo", ctypes.c_int64), ("count", ctypes.c_int64),
+                ("max_fint", ctypes.c_int64)]
+
+    @property
+    def sum_fint(self) -> int:
+        return (self.sum_hi << 64) | (self.sum_lo & (2**64 - 1))
 
 
 class ubqp_stats(ctypes.Structure):
@@ -64,6 +77,9 @@ def load_library(path: Path | str | None = None):
         "ubqp_ascend": ([P, P, i64, i32, P, P, P, P], ctypes.c_int),
         "ubqp_sync": ([P], ctypes.c_int),
         "ubqp_query": ([P, ctypes.c_int, ctypes.POINTER(i64)], ctypes.c_int),
+        "ubqp_load_Q_real": ([P, i32, ctypes.c_int, P, i64], ctypes.c_int),
+        "ubqp_eval_batch_real": ([P, P, P], ctypes.c_int),
+        "ubqp_screen_real": ([P, dbl, dbl, dbl, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -169,6 +185,30 @@ class Ubqp:
                best_key_out=None):
         self._ck(self.lib.ubqp_ascend(self.h, _ptr(slots), m, max_flips, _ptr(f_out), _ptr(flips_out),
                                       _ptr(bits_out), _ptr(best_key_out)))
+
+    # ---- real-valued Q (a4')
+    def load_Q_real(self, Q, k_max: int):
+        if isinstance(Q, np.ndarray):
+            dt = UBQP_F32 if Q.dtype == np.float32 else UBQP_F64
+            Q = np.ascontiguousarray(Q, dtype=np.float32 if dt == UBQP_F32 else np.float64)
+        else:
+            import torch
+            dt = UBQP_F32 if Q.dtype == torch.float32 else UBQP_F64
+        self._ck(self.lib.ubqp_load_Q_real(self.h, Q.shape[0], dt, _ptr(Q), k_max))
+
+    @property
+    def real_exp(self) -> int:
+        return self.query(Q_REAL_EXP)
+
+    def eval_batch_real(self, f_out=None, stats_out=None):
+        self._ck(self.lib.ubqp_eval_batch_real(self.h, _ptr(f_out), _ptr(stats_out)))
+
+    def screen_real(self, lam: float, mean: float, max_value: float, surv_out):
+        m = ctypes.c_int64()
+        T = ctypes.c_double()
+        self._ck(self.lib.ubqp_screen_real(self.h, float(lam), float(mean), float(max_value), _ptr(surv_out),
+                                           ctypes.byref(m), ctypes.byref(T)))
+        return m.value, T.value
 
     def sync(self):
         self._ck(self.lib.ubqp_sync(self.h))

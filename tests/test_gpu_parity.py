@@ -260,7 +260,7 @@ def test_full_size_sampled(n, K, kind):
 
 @pytest.mark.parametrize("n", [5000, 7000])
 def test_ascend_full_size(n):
-    """The bench shapes (64x5 at n = 5000, 96x5 at n = 7000), exact against the oracle."""
+    """The bench shapes (64x7 at n = 5000 and n = 7000), exact against the oracle."""
     Q = generate_Q(n, 1.0, seed=4)
     K = 24
     u = _handle_with(Q, K)
@@ -280,7 +280,7 @@ def test_ascend_full_size(n):
     assert np.array_equal(unpack_bits(b_o, n), Xr)
 
 
-@pytest.mark.parametrize("shape", ["32,5", "64,4", "64,5", "96,4", "128,4", "160,5"])
+@pytest.mark.parametrize("shape", ["32,5", "32,7", "64,5", "64,7", "96,5", "128,4", "160,7"])
 def test_ascend_forced_shapes(shape, monkeypatch):
     n, K = 2500, 40
     Q = generate_Q(n, 0.5, seed=8)

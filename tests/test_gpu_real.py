@@ -1,0 +1,114 @@
+"""GPU parity of the real-valued Q path (SURVEY §8(a) a4'): int8 limb planes on the tensor
+cores, exact integer combine, against the exactly rounded oracle O9.
+
+Tolerance (R3, north_star "within a relative 1e-5 for floating-point Q"):
+    |f_gpu - f_ref| <= 1e-5 * max(|f_ref|, s_k),  s_k = sqrt(sum_{i,j in S} Q_ij^2),
+and the tighter analytic bound of the 28-bit fixed point (include/ubqp.h):
+    |f_gpu - f_ref| <= |S|^2 * 2^-(e+1) + |f_ref| * 2^-52.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from inputs import generate_Q, generate_Q_real, pack_bits, unpack_bits
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1706_00037_b200 import Ubqp, UbqpError, ubqp_stats_real  # noqa: E402
+from paper_1706_00037_b200.build import build_lib  # noqa: E402
+
+build_lib()
+
+
+def _check(Q, X, f, e):
+    Q = np.asarray(Q, dtype=np.float64)
+    for k in range(X.shape[0]):
+        S = np.flatnonzero(X[k])
+        ref = oracle.xQx_real(Q, X[k])
+        sk = float(np.sqrt((Q[np.ix_(S, S)] ** 2).sum())) if S.size else 0.0
+        err = abs(f[k] - ref)
+        assert err <= 1e-5 * max(abs(ref), sk), (k, f[k], ref)
+        assert err <= S.size ** 2 * 2.0 ** (-(e + 1)) + abs(ref) * 2.0 ** -52 + 1e-300, (k, err)
+
+
+@pytest.mark.parametrize("n", [1, 3, 65, 300, 1100, 2500])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_eval_real(n, dtype):
+    Q = generate_Q_real(n, 0.7, seed=n, dtype=dtype)
+    K = 40 if n >= 1100 else 150
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    u.random(n + 1, K)
+    f = np.zeros(K, np.float64)
+    st = ubqp_stats_real()
+    u.eval_batch_real(f, st)
+    X = oracle.random_solutions(n, n + 1, K)
+    _check(Q, X, f, u.real_exp)
+    # integer-image stats are exact: sum of f * 2^e equals the int128 sum
+    fint = [int(round(v * 2.0 ** u.real_exp)) for v in f]
+    assert st.count == K and st.sum_fint == sum(fint) and st.max_fint == max(fint)
+
+
+def test_real_equals_integer_path_on_integer_Q():
+    n, K = 500, 300
+    Q = generate_Q(n, 0.5, seed=12)
+    u = Ubqp(0)
+    u.load_Q_real(Q.astype(np.float64), K)
+    u.random(3, K)
+    f = np.zeros(K, np.float64)
+    u.eval_batch_real(f)
+    assert np.array_equal(f, oracle.eval_batch(Q, oracle.random_solutions(n, 3, K), nthreads=8).astype(np.float64))
+
+
+def test_real_screen_and_first_derivative():
+    n, K = 400, 2000
+    Q = generate_Q_real(n, 0.5, seed=4)
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    b = np.zeros(u.W64, np.uint64)
+    u.first_derivative(b)
+    assert np.array_equal(unpack_bits(b, n)[0], oracle.first_derivative_start_real(Q))
+    u.diversify(b, 0, K)
+    f = np.zeros(K, np.float64)
+    u.eval_batch_real(f)
+    mean, mx = float(f.mean()), float(f.max())
+    surv = np.zeros(K, np.int32)
+    for lam in (0.0, 0.5, 0.9):
+        m, T = u.screen_real(lam, mean, mx, surv)
+        assert T == mean + lam * (mx - mean)
+        assert surv[:m].tolist() == np.flatnonzero(f > T).tolist()
+
+
+def test_real_errors():
+    u = Ubqp(0)
+    with pytest.raises(UbqpError) as e:
+        u.load_Q_real(np.array([[1.0, 2.0], [2.5, 1.0]]), 4)
+    assert e.value.code == 2
+    with pytest.raises(UbqpError) as e:
+        u.load_Q_real(np.array([[np.nan]]), 4)
+    assert e.value.code == 3
+    u.load_Q_real(np.array([[1.5]]), 4)
+    u.random(0, 1)
+    with pytest.raises(UbqpError) as e:
+        u.eval_batch(0)                       # integer-only entry point
+    assert e.value.code == 4
+    f = np.zeros(1)
+    u.eval_batch_real(f)
+    assert f[0] in (0.0, 1.5)
+
+
+@pytest.mark.parametrize("n", [7000])
+def test_real_full_size_sampled(n):
+    Q = generate_Q_real(n, 1.0, seed=4, dtype=np.float32)
+    K = 4096
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    u.random(4, K)
+    f = np.zeros(K, np.float64)
+    u.eval_batch_real(f)
+    idx = np.array([0, 1, 777, K - 1])
+    X = oracle.random_solutions(n, 4, K)[idx]
+    _check(Q, X, f[idx], u.real_exp)

@@ -348,3 +348,29 @@ def test_pack_unpack_roundtrip():
         assert np.array_equal(unpack_bits(B, n), X)
         j = n - 1
         assert ((B[:, j >> 6] >> np.uint64(j & 63)) & np.uint64(1)).astype(np.uint8).tolist() == X[:, j].tolist()
+
+
+# ---------------------------------------------------------------- O9 real Q
+def test_real_oracle_reduces_to_integer_oracle():
+    """On integer-valued float Q the exactly rounded sum is the exact integer xQx (O1)."""
+    rng = np.random.default_rng(19)
+    Q = generate_Q(60, 0.5, seed=3)
+    X = rng.integers(0, 2, size=(20, 60)).astype(np.uint8)
+    assert np.array_equal(oracle.eval_batch_real(Q.astype(np.float64), X),
+                          oracle.eval_batch(Q, X).astype(np.float64))
+    assert np.array_equal(oracle.first_derivative_start_real(Q.astype(np.float64)),
+                          oracle.first_derivative_start(Q))
+
+
+def test_real_oracle_closed_forms_and_exact_rounding():
+    from inputs import generate_Q_real
+    Q = generate_Q_real(40, 1.0, seed=5)
+    n = 40
+    assert oracle.xQx_real(Q, np.zeros(n)) == 0.0
+    for i in (0, 17, 39):
+        assert oracle.xQx_real(Q, np.eye(n)[i]) == Q[i, i]
+    # exact rounding: compare against the exact rational sum
+    x = np.random.default_rng(1).integers(0, 2, size=n)
+    S = np.flatnonzero(x)
+    exact = sum(Fraction(float(v)) for v in Q[np.ix_(S, S)].ravel())
+    assert oracle.xQx_real(Q, x) == float(exact)
