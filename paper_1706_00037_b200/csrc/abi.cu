@@ -103,11 +103,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2-D int8 tensor map: inner dim `cols` bytes (contiguous), outer `rows`, box 128 x box_rows,
 // 128-byte swizzle (the UMMA K-major SW128 canonical layout).
-bool encode_map(CUtensorMap *m, void *base, uint64_t cols, uint64_t rows, uint32_t box_rows) {
+bool encode_map(CUtensorMap *m, void *base, uint64_t cols, uint64_t rows, uint32_t box_rows,
+                uint64_t ld = 0) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols};
+    cuuint64_t strides[1] = {ld ? ld : cols};
     cuuint32_t box[2] = {128u, box_rows};
     cuuint32_t estr[2] = {1u, 1u};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
@@ -255,11 +256,12 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     h->n_pad = (n + ubqp::kNPadAlign - 1) / ubqp::kNPadAlign * ubqp::kNPadAlign;
     h->q_rows = (n + ubqp::kQRowAlign - 1) / ubqp::kQRowAlign * ubqp::kQRowAlign;
     h->W64 = (n + 63) / 64;
-    std::vector<int8_t> q8(static_cast<size_t>(h->q_rows) * h->n_pad, 0);
+    h->q_ld = ubqp::ascend_capacity(h->n_pad);
+    std::vector<int8_t> q8(static_cast<size_t>(h->q_rows) * h->q_ld, 0);
     std::vector<int32_t> dg(h->q_rows, 0);
     for (int i = 0; i < n; ++i) {
         for (int j = 0; j < n; ++j)
-            q8[static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
+            q8[static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
         dg[i] = Qh[static_cast<int64_t>(i) * n + i];
     }
     if (cudaMalloc(&h->Q8, q8.size()) != cudaSuccess || cudaMalloc(&h->diag, dg.size() * 4) != cudaSuccess ||
@@ -285,7 +287,7 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     }
     CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
     if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM) ||
-        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN)) {
+        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN, h->q_ld)) {
         free_all(*h);
         return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
     }
@@ -549,7 +551,8 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
     h->W64 = (n + 63) / 64;
     h->real = true;
     h->q_exp = e;
-    const size_t plane = static_cast<size_t>(h->q_rows) * h->n_pad;
+    h->q_ld = ubqp::ascend_capacity(h->n_pad);
+    const size_t plane = static_cast<size_t>(h->q_rows) * h->q_ld;
     std::vector<int8_t> L(plane * ubqp::kSlices, 0);
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
@@ -557,7 +560,7 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
             for (int sl = 0; sl < ubqp::kSlices; ++sl) {
                 const long long r = ((v % 128) + 128) % 128;
                 const long long d = r >= 64 ? r - 128 : r;         // balanced digit in [-64, 63]
-                L[sl * plane + static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(d);
+                L[sl * plane + static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(d);
                 v = (v - d) / 128;
             }
         }
@@ -583,7 +586,7 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
     CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));
     for (int sl = 0; sl < ubqp::kSlices; ++sl) {
         CK(cudaMemcpy(h->Qs[sl], L.data() + sl * plane, plane, cudaMemcpyHostToDevice));
-        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN)) {
+        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN, h->q_ld)) {
             free_all(*h);
             return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
         }

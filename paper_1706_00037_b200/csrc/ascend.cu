@@ -88,9 +88,9 @@ __device__ __forceinline__ void owner_fix(int (&K)[NCH][16], uint32_t (&m)[NCH][
 #define UBQP_CASE8(B) UBQP_CASE(B) UBQP_CASE(B + 1) UBQP_CASE(B + 2) UBQP_CASE(B + 3) \
                       UBQP_CASE(B + 4) UBQP_CASE(B + 5) UBQP_CASE(B + 6) UBQP_CASE(B + 7)
 
-template <int BLOCK, int NCH, int MINB>
+template <int BLOCK, int NCH, int MINB, bool FULL>
 __global__ void __launch_bounds__(BLOCK, MINB)
-ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int W64,
+ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int q_ld, int W64,
               int64_t k_local, int rank, int world, const int8_t *__restrict__ Q8,
               const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
               const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out,
@@ -145,7 +145,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
 #pragma unroll
         for (int e = 0; e < 16; ++e) run = max(run, K[c][e]);
 
-    const int8_t *qbase = Q8 + 16 * t;        // + kstar*n_pad + c*CHUNK per step
+    const int8_t *qbase = Q8 + 16 * t;        // + kstar*q_ld + c*CHUNK per step
     bool cvalid[NCH];
 #pragma unroll
     for (int c = 0; c < NCH; ++c) cvalid[c] = c * A::CHUNK + 16 * t < n_pad;
@@ -192,11 +192,15 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         const int C = xk ? -512 : 512;          // 512 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;
-        const int8_t *qrow = qbase + static_cast<int64_t>(kstar) * n_pad;
+        const uint4 *qrow = reinterpret_cast<const uint4 *>(qbase + static_cast<int64_t>(kstar) * q_ld);
         uint4 w[NCH];
 #pragma unroll
-        for (int c = 0; c < NCH; ++c)
-            w[c] = cvalid[c] ? __ldg(reinterpret_cast<const uint4 *>(qrow + c * A::CHUNK)) : make_uint4(0, 0, 0, 0);
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (FULL)      // capacity <= q_ld: every chunk lies in the zero-padded row
+                w[c] = __ldg(qrow + c * (A::CHUNK / 16));
+            else
+                w[c] = cvalid[c] ? __ldg(qrow + c * (A::CHUNK / 16)) : make_uint4(0, 0, 0, 0);
+        }
         if (((kstar % A::CHUNK) >> 4) == t) {
             const int li = (kstar / A::CHUNK) * 16 + (kstar & 15);
             const int x_new = xk ^ 1;
@@ -276,23 +280,52 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
 template <int BLOCK, int NCH>
 void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_dev,
                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
+    const bool full = 16 * BLOCK * NCH <= c.q_ld;
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
     // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
     constexpr int kRegs = NCH >= 6 ? 256 : 24 * NCH + 48;
     constexpr int kMinBlocks = (65536 / (BLOCK * kRegs)) < 1 ? 1 : 65536 / (BLOCK * kRegs);
-    ascend_kernel<BLOCK, NCH, kMinBlocks><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
-        slots, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f, c.Xb,
-        f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
+    if (full)
+        ascend_kernel<BLOCK, NCH, kMinBlocks, true><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
+            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+            c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
+    else
+        ascend_kernel<BLOCK, NCH, kMinBlocks, false><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
+            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+            c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
 }
 
 }  // namespace
 
-// Shape: NCH = 7 sixteen-variable chunks per thread (112 register keys) and the smallest
-// multiple of 32 threads covering n_pad (64 threads at n = 7000: 98% of the lanes carry a
-// variable); below 3584 variables one warp with fewer chunks.  Fewer, fuller threads
-// amortise the per-step argmax exchange (measured: 96x5 306 ms, 64x7 277 ms at config 4).
+// Shape: the instantiated (BLOCK, NCH) with the least capacity 16*BLOCK*NCH >= n_pad, ties
+// to more variables per thread (64x7 at n = 7000: 98% of the lanes carry a variable; 64x5 at
+// n = 5000).  Fewer, fuller threads amortise the per-step argmax exchange (measured at
+// config 4: 96x5 306 ms, 64x7 277 ms).  Q8 rows are padded with zeros to this capacity
+// (Ctx::q_ld) so the default shape loads every chunk unpredicated.
 // UBQP_ASC_CFG="BLOCK,NCH" forces a shape (tuning sweeps, tools/asc_sweep.py).
 // Returns 0 on success, 1 if n is outside the instantiated range.
+static const int kShapes[][2] = {{32, 1}, {32, 2}, {32, 3}, {32, 4}, {32, 5}, {32, 6}, {32, 7},
+                                  {64, 5}, {64, 6}, {64, 7}, {96, 5}, {96, 6}, {96, 7},
+                                  {128, 5}, {128, 6}, {128, 7}, {160, 6}, {160, 7}};
+// the instantiated shape with the smallest capacity >= n_pad (ties: more variables per thread)
+static void default_shape(int np, int &b, int &nch) {
+    int best = -1;
+    for (int i = 0; i < static_cast<int>(sizeof(kShapes) / sizeof(kShapes[0])); ++i) {
+        const int cap = 16 * kShapes[i][0] * kShapes[i][1];
+        if (cap < np) continue;
+        if (best < 0) { best = i; continue; }
+        const int bcap = 16 * kShapes[best][0] * kShapes[best][1];
+        if (cap < bcap || (cap == bcap && kShapes[i][1] > kShapes[best][1])) best = i;
+    }
+    b = kShapes[best][0];
+    nch = kShapes[best][1];
+}
+int ascend_capacity(int n_pad) {
+    int b, nch;
+    default_shape(n_pad, b, nch);
+    return 16 * b * nch;
+}
+
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                   int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     if (m <= 0) return 0;
@@ -302,8 +335,7 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
         if (sscanf(env, "%d,%d", &fb, &fn) != 2 || fb * 16 * fn < np) fb = fn = 0;
     }
     int db, dn;   // default shape
-    if (np <= 3584) { db = 32; dn = (np + 511) / 512; }
-    else { db = 32 * ((np + 32 * 112 - 1) / (32 * 112)); dn = 7; }
+    default_shape(np, db, dn);
     if (!fb) { fb = db; fn = dn; }
 #define UBQP_ASC(B, N)                                                                          \
     if (fb == B && fn == N) {                                                                   \
@@ -313,8 +345,9 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
     }
 #define UBQP_ASC_ALL                                                                                  \
     UBQP_ASC(32, 1) UBQP_ASC(32, 2) UBQP_ASC(32, 3) UBQP_ASC(32, 4) UBQP_ASC(32, 5) UBQP_ASC(32, 6)   \
-    UBQP_ASC(32, 7) UBQP_ASC(64, 7) UBQP_ASC(96, 7) UBQP_ASC(128, 7) UBQP_ASC(160, 7)                 \
-    UBQP_ASC(64, 5) UBQP_ASC(96, 5) UBQP_ASC(128, 4) UBQP_ASC(128, 5)
+    UBQP_ASC(32, 7) UBQP_ASC(64, 5) UBQP_ASC(64, 6) UBQP_ASC(64, 7) UBQP_ASC(96, 5) UBQP_ASC(96, 6)   \
+    UBQP_ASC(96, 7) UBQP_ASC(128, 5) UBQP_ASC(128, 6) UBQP_ASC(128, 7) UBQP_ASC(160, 6)               \
+    UBQP_ASC(160, 7)
     UBQP_ASC_ALL
     fb = db;                       // a forced shape that is not instantiated: use the default
     fn = dn;

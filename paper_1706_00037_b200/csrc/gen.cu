@@ -122,7 +122,7 @@ struct Planes {
     int count;
 };
 
-__global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, int n, int n_pad, int W64,
+__global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, int n, int n_pad, int q_ld, int W64,
                                                                uint32_t *__restrict__ bits32) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, in
         for (int pl = planes.count - 1; pl >= 0; --pl) {
             int s = 0;
             if (i < n)
-                for (int j = lane; j < n_pad; j += 32) s += planes.p[pl][static_cast<int64_t>(i) * n_pad + j];
+                for (int j = lane; j < n_pad; j += 32) s += planes.p[pl][static_cast<int64_t>(i) * q_ld + j];
             s = __reduce_add_sync(0xffffffffu, s);
             tot = tot * 128 + s;
         }
@@ -182,7 +182,7 @@ void launch_first_derivative(Ctx &c, uint64_t *bits_dev) {
         pl.count = 1;
     }
     first_derivative_kernel<<<(warps * 32 + 255) / 256, 256, 0, c.stream>>>(
-        pl, c.n, c.n_pad, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
+        pl, c.n, c.n_pad, c.q_ld, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
     ++c.launches;
 }
 

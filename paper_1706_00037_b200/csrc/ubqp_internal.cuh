@@ -32,7 +32,8 @@ struct Ctx {
 
     // instance
     int n = 0, n_pad = 0, q_rows = 0, W64 = 0;
-    int8_t *Q8 = nullptr;        // [q_rows][n_pad] row-major, zero padded; row k = column k (Q = Q^t)
+    int q_ld = 0;                // Q8 row stride >= n_pad: the ascent's register capacity (zero tail)
+    int8_t *Q8 = nullptr;        // [q_rows][q_ld] row-major, zero padded; row k = column k (Q = Q^t)
     int32_t *diag = nullptr;     // [q_rows]
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     // batch workspace
@@ -78,6 +79,7 @@ void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
 void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);
 void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
 // ascend.cu
+int ascend_capacity(int n_pad);   // variables covered by the default ascent shape (>= n_pad)
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,
                   int64_t *f_dev, int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
 

@@ -280,7 +280,7 @@ def test_ascend_full_size(n):
     assert np.array_equal(unpack_bits(b_o, n), Xr)
 
 
-@pytest.mark.parametrize("shape", ["32,5", "32,7", "64,5", "64,7", "96,5", "128,4", "160,7"])
+@pytest.mark.parametrize("shape", ["32,5", "32,7", "64,5", "64,7", "96,5", "96,6", "128,5", "160,7"])
 def test_ascend_forced_shapes(shape, monkeypatch):
     n, K = 2500, 40
     Q = generate_Q(n, 0.5, seed=8)
