@@ -294,3 +294,17 @@ def test_ascend_forced_shapes(shape, monkeypatch):
     X0 = oracle.random_solutions(n, 9, K)
     Xr, fr, _ = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0, nthreads=8), 100000, nthreads=8)
     assert np.array_equal(f_o, fr) and np.array_equal(unpack_bits(b_o, n), Xr)
+
+
+@pytest.mark.parametrize("n,K,rounds,lam", [(50, 1000, 3, 0.5), (300, 2000, 2, 0.3), (1100, 600, 2, 0.7)])
+def test_multistart_rounds_match_oracle(n, K, rounds, lam):
+    """The composed product round (MultiStart: sampling mean, first-derivative incumbent,
+    diversify/eval/screen/ascend/best record; O8) against the oracle's run_rounds."""
+    from paper_1706_00037_b200.multistart import MultiStart
+    Q = generate_Q(n, 0.1 if n == 50 else 0.5, seed=n)
+    ms = MultiStart(Q, K, lam=lam, max_flips=10 * n)
+    best, bits, traj = ms.run(rounds, sample_seed=7)
+    obest, ox, otraj = oracle.run_rounds(Q, K, rounds, lam, 10 * n, sample_seed=7, nthreads=8)
+    assert best == obest and traj == otraj
+    got = unpack_bits(bits.cpu().numpy().view(np.uint64), n)[0]
+    assert np.array_equal(got, ox)
