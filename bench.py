@@ -340,6 +340,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if world == 1 and not args.no_table1:
         out["table1_eval_1000"] = table1_eval(local_rank)
         out["real_q_eval"] = real_q_eval(local_rank)
+        out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
     print(json.dumps(out), flush=True)
 
 
@@ -418,6 +419,33 @@ def table1_eval(device):
                         "paper_gtx780ti_s": paper_s, "speedup_vs_paper": paper_s / (us * 1e-6)}
         u.close()
     return res
+
+
+def f_only_eval(device, cfg, Q):
+    """f-only evaluation of the config-4 batch (no gains): the triangular GEMM (SURVEY §8(f)
+    NEXT-1), algorithmic work n(n+1) ops per evaluation."""
+    import torch
+
+    from paper_1706_00037_b200 import Ubqp
+    n, K = cfg["n"], cfg["K"]
+    u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+    u.load_Q(Q, K)
+    u.random(4, K)
+    f = torch.zeros(K, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        u.eval_batch(0, f)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 5
+    e0.record()
+    for _ in range(reps):
+        u.eval_batch(0, f)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    u.close()
+    return {"n": n, "K": K, "ms": ms, "evals_per_s": K / (ms * 1e-3),
+            "algorithmic_tops": n * (n + 1) * K / (ms * 1e-3) / 1e12,
+            "note": "n(n+1) ops per evaluation (upper triangle incl. diagonal)"}
 
 
 def real_q_eval(device):

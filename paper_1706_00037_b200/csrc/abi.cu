@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -79,7 +80,7 @@ void free_batch(Ctx &c) {
 
 void free_all(Ctx &c) {
     free_batch(c);
-    dfree(c.Q8); dfree(c.diag); dfree(c.seed); dfree(c.scratch64);
+    dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
     dfree(c.fs); dfree(c.fint); dfree(c.freal);
     c.real = false;
@@ -153,7 +154,7 @@ int run_eval(ubqp_t h, bool emit_gains) {
     }
     const int64_t k = h->k_local;
     if (k > 0) CK(cudaMemsetAsync(h->f, 0, k * sizeof(int64_t), h->stream));
-    ubqp::launch_eval_tc(*h, k, emit_gains);
+    ubqp::launch_eval_tc(*h, k, emit_gains, nullptr, nullptr, h->sym_eval && h->Q8L && !emit_gains);
     CK_LAUNCH("eval_tc_kernel");
     ubqp::launch_stats(*h, k, h->scratch64);
     CK_LAUNCH("stats_kernel");
@@ -197,6 +198,7 @@ int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
         delete h;
         return UBQP_E_INVALID;   // built for sm_100a (B200) only
     }
+    if (const char *env = getenv("UBQP_FULL_EVAL")) h->sym_eval = env[0] == '0';
     if (cuda_stream) {
         h->stream = static_cast<cudaStream_t>(cuda_stream);
     } else {
@@ -259,18 +261,24 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     h->q_ld = ubqp::ascend_capacity(h->n_pad);
     std::vector<int8_t> q8(static_cast<size_t>(h->q_rows) * h->q_ld, 0);
     std::vector<int32_t> dg(h->q_rows, 0);
+    std::vector<int8_t> q8l(static_cast<size_t>(h->q_rows) * h->n_pad, 0);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j <= i; ++j)
+            q8l[static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
     for (int i = 0; i < n; ++i) {
         for (int j = 0; j < n; ++j)
             q8[static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
         dg[i] = Qh[static_cast<int64_t>(i) * n + i];
     }
     if (cudaMalloc(&h->Q8, q8.size()) != cudaSuccess || cudaMalloc(&h->diag, dg.size() * 4) != cudaSuccess ||
+        cudaMalloc(&h->Q8L, q8l.size()) != cudaSuccess ||
         cudaMalloc(&h->seed, h->W64 * sizeof(uint64_t)) != cudaSuccess) {
         cudaGetLastError();
         free_all(*h);
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate Q");
     }
     CK(cudaMemcpy(h->Q8, q8.data(), q8.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->Q8L, q8l.data(), q8l.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->diag, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
     // batch workspace
     h->k_max = k_max;
@@ -287,7 +295,8 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     }
     CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
     if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM) ||
-        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN, h->q_ld)) {
+        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
+        !encode_map(&h->tmap_Q8L, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN)) {
         free_all(*h);
         return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
     }

@@ -28,6 +28,10 @@ constexpr uint32_t kTmemCols = 2 * kBN;             // two 128 x 256 s32 accumul
 constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
 constexpr uint32_t kIdesc = dev::idesc_i8(kBM, kBN);
 
+// SYM (f only, NEXT-1 of SURVEY §8(f)): B = the lower triangle of Q (row j keeps Q_ji, i <= j),
+// so tile column block J needs only K blocks covering rows i < 256(J+1): ~(n+256)/(2n) of the
+// MMAs.  f = sum_j x_j (2 Y^U_j - Q_jj) with Y^U_j = sum_{i<=j} x_i Q_ij  (Q = Q^t).
+template <bool SYM>
 __global__ void __launch_bounds__(kThreads, 1)
 eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ,
                int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
@@ -76,8 +80,10 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             uint32_t phase = 0;
             for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 const int m0 = static_cast<int>(tile / num_n_tiles) * kBM;
-                const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
-                for (int kb = 0; kb < num_k_blocks; ++kb) {
+                const int nt = static_cast<int>(tile % num_n_tiles);
+                const int n0 = nt * kBN;
+                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
+                for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     mbar_arrive_expect_tx(&full[stage], kStageBytes);
                     tma_load_2d(sA + stage * kABytes, &tmX, kb * kBK, m0, &full[stage], pol_x);
@@ -97,7 +103,9 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
                 mbar_wait(&tempty[acc], acc_phase ^ 1u);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
-                for (int kb = 0; kb < num_k_blocks; ++kb) {
+                const int nt = static_cast<int>(tile % num_n_tiles);
+                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
+                for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
@@ -140,10 +148,24 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
                 uint32_t bits = 0;
                 if (row_ok && (col0 >> 6) < W64)
                     bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
+                if constexpr (SYM) {
+                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
-                if (emit_gains && row_ok && col0 < n_pad) {
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const int4 d = __ldg(dg + i4);
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = 4 * i4 + e;
+                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
+                }
+                if (!SYM && emit_gains && row_ok && col0 < n_pad) {
                     const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
                     int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
 #pragma unroll
@@ -219,10 +241,13 @@ bool g_attr_set = false;
 
 }  // namespace
 
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q, int64_t *f_out) {
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q, int64_t *f_out,
+                    bool sym) {
     if (k <= 0) return;
     if (!g_attr_set) {
-        cudaFuncSetAttribute(eval_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kSmemBytes));
+        cudaFuncSetAttribute(eval_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes));
         g_attr_set = true;
     }
@@ -231,9 +256,14 @@ void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_
     const int64_t num_m_tiles = (k + kBM - 1) / kBM;
     const int64_t num_tiles = num_m_tiles * num_n_tiles;
     const int grid = static_cast<int>(num_tiles < c.num_sms ? num_tiles : c.num_sms);
-    eval_tc_kernel<<<grid, kThreads, kSmemBytes, c.stream>>>(
-        c.tmap_X8, tmap_q ? *tmap_q : c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks,
-        num_tiles, c.Xb, c.diag, f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+    if (sym && !emit_gains)
+        eval_tc_kernel<true><<<grid, kThreads, kSmemBytes, c.stream>>>(
+            c.tmap_X8, c.tmap_Q8L, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb,
+            c.diag, f_out ? f_out : c.f, nullptr, 0);
+    else
+        eval_tc_kernel<false><<<grid, kThreads, kSmemBytes, c.stream>>>(
+            c.tmap_X8, tmap_q ? *tmap_q : c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks,
+            num_tiles, c.Xb, c.diag, f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
     ++c.launches;
 }
 

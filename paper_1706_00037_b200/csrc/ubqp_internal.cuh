@@ -52,6 +52,9 @@ struct Ctx {
     int32_t *asc_slots = nullptr; int64_t asc_cap = 0;
     // TMA descriptors (64 B each, passed by value as __grid_constant__)
     CUtensorMap tmap_X8{}, tmap_Q8{};
+    int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
+    CUtensorMap tmap_Q8L{};
+    bool sym_eval = true;        // f-only evaluations use the triangular GEMM (UBQP_FULL_EVAL disables)
     // real-valued Q (a4'): Q~ = 2^-q_exp * sum_s 128^s L_s, int8 limb planes L_s in [-64, 63]
     bool real = false;
     int q_exp = 0;
@@ -72,7 +75,7 @@ void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
 void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer or real planes
 // eval_tc.cu
 void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q = nullptr,
-                    int64_t *f_out = nullptr);
+                    int64_t *f_out = nullptr, bool sym = false);
 void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev);
 void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
 // screen.cu

@@ -308,3 +308,22 @@ def test_multistart_rounds_match_oracle(n, K, rounds, lam):
     assert best == obest and traj == otraj
     got = unpack_bits(bits.cpu().numpy().view(np.uint64), n)[0]
     assert np.array_equal(got, ox)
+
+
+@pytest.mark.parametrize("n", [1, 2, 200, 257, 513, 2500])
+def test_symmetric_and_full_eval_agree(n, monkeypatch):
+    """f-only evaluations use the triangular GEMM (NEXT-1); UBQP_FULL_EVAL=1 forces the full
+    one.  Both must equal the oracle exactly."""
+    Q = generate_Q(n, 0.6, seed=n + 40)
+    K = 300
+    X = oracle.random_solutions(n, 21, K)
+    ref = oracle.eval_batch(Q, X, nthreads=8)
+    for full in ("0", "1"):
+        monkeypatch.setenv("UBQP_FULL_EVAL", full)
+        u = _handle_with(Q, K)
+        u.random(21, K)
+        f = np.zeros(K, np.int64)
+        st = ubqp_stats()
+        u.eval_batch(0, f, st)
+        assert np.array_equal(f, ref), full
+        assert st.max_key == oracle.stats(ref)[2]
