@@ -154,7 +154,7 @@ int run_eval(ubqp_t h, bool emit_gains) {
     }
     const int64_t k = h->k_local;
     if (k > 0) CK(cudaMemsetAsync(h->f, 0, k * sizeof(int64_t), h->stream));
-    ubqp::launch_eval_tc(*h, k, emit_gains, nullptr, nullptr, h->sym_eval && h->Q8L && !emit_gains);
+    ubqp::launch_eval_tc(*h, k, emit_gains, -1, nullptr, h->sym_eval && h->Q8L && !emit_gains);
     CK_LAUNCH("eval_tc_kernel");
     ubqp::launch_stats(*h, k, h->scratch64);
     CK_LAUNCH("stats_kernel");
@@ -199,6 +199,7 @@ int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
         return UBQP_E_INVALID;   // built for sm_100a (B200) only
     }
     if (const char *env = getenv("UBQP_FULL_EVAL")) h->sym_eval = env[0] == '0';
+    if (const char *env = getenv("UBQP_EVAL_2SM")) h->eval_pair = env[0] != '0';
     if (cuda_stream) {
         h->stream = static_cast<cudaStream_t>(cuda_stream);
     } else {
@@ -296,7 +297,9 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
     if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM) ||
         !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
-        !encode_map(&h->tmap_Q8L, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN)) {
+        !encode_map(&h->tmap_Q8L, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN) ||
+        !encode_map(&h->tmap_Q8_h, h->Q8, h->n_pad, h->q_rows, ubqp::kBN / 2, h->q_ld) ||
+        !encode_map(&h->tmap_Q8L_h, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN / 2)) {
         free_all(*h);
         return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
     }
@@ -595,7 +598,8 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
     CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));
     for (int sl = 0; sl < ubqp::kSlices; ++sl) {
         CK(cudaMemcpy(h->Qs[sl], L.data() + sl * plane, plane, cudaMemcpyHostToDevice));
-        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN, h->q_ld)) {
+        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
+            !encode_map(&h->tmap_Qs_h[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN / 2, h->q_ld)) {
             free_all(*h);
             return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
         }
@@ -618,7 +622,7 @@ int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out) {
     if (k > 0) {
         CK(cudaMemsetAsync(h->fs, 0, ubqp::kSlices * h->k_max * sizeof(int64_t), h->stream));
         for (int sl = 0; sl < ubqp::kSlices; ++sl) {
-            ubqp::launch_eval_tc(*h, k, false, &h->tmap_Qs[sl], h->fs + sl * h->k_max);
+            ubqp::launch_eval_tc(*h, k, false, sl, h->fs + sl * h->k_max);
             CK_LAUNCH("eval_tc_kernel (plane)");
         }
     }

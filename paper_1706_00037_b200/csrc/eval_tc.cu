@@ -199,6 +199,191 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     }
 }
 
+// ---------------------------------------------------------------- CTA-pair variant
+// cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with M = 256 MMAs
+// issued by the leader; each CTA stages its 128 rows of X and its 128 rows of Q per K block
+// (32 KB per stage instead of 48 KB), so the shared-memory and L2 traffic per MAC halves for
+// B.  Accumulators: each CTA's TMEM holds its 128 rows x 256 columns (two buffers).
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairStageBytes = 2 * kABytes;                    // 16 KB A + 16 KB B
+constexpr size_t kPairSmemBytes = static_cast<size_t>(kPairStages) * kPairStageBytes + 1024 + 256;
+constexpr uint32_t kIdescPair = dev::idesc_i8(2 * kBM, kBN);
+
+template <bool SYM>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQh,
+                    int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
+                    const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
+                    int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains) {
+    using namespace dev;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                ~static_cast<uintptr_t>(1023));
+    uint8_t *sA = smem;
+    uint8_t *sB = smem + kPairStages * kABytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kPairStages * kPairStageBytes);
+    uint64_t *empty = full + kPairStages;
+    uint64_t *tfull = empty + kPairStages;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kPairStages; ++s) {
+            mbar_init(&full[s], 1);           // the leader's expect_tx; both CTAs' bytes land here
+            mbar_init(&empty[s], 1);          // multicast commit of the leader's MMAs
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);          // multicast commit
+            mbar_init(&tempty[a], 8);         // 4 epilogue warps x 2 CTAs (leader's copy is used)
+        }
+        fence_mbar_init();
+        tma_prefetch(&tmX);
+        tma_prefetch(&tmQh);
+    }
+    if (warp == 1) tmem_alloc_cg2(tmem_slot, kTmemCols);
+    tc_fence_before();
+    cluster_sync();                           // barriers of both CTAs initialised, TMEM allocated
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs: own half of A and of B)
+            const uint64_t pol_q = policy_evict_last();
+            const uint64_t pol_x = policy_evict_normal();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+                const int m0 = static_cast<int>(tile / num_n_tiles) * (2 * kBM) + static_cast<int>(rank) * kBM;
+                const int nt = static_cast<int>(tile % num_n_tiles);
+                const int n0 = nt * kBN + static_cast<int>(rank) * (kBN / 2);
+                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
+                for (int kb = 0; kb < kbs; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1u);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
+                    const uint32_t fb = mapa_u32(&full[stage], 0);
+                    tma_load_2d_cg2(sA + stage * kABytes, &tmX, kb * kBK, m0, fb, pol_x);
+                    tma_load_2d_cg2(sB + stage * kABytes, &tmQh, kb * kBK, n0, fb, pol_q);
+                    if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ---------------- MMA issuer (leader only): M = 256 across the pair
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
+                const int nt = static_cast<int>(tile % num_n_tiles);
+                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
+                for (int kb = 0; kb < kbs; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
+                    const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kABytes));
+#pragma unroll
+                    for (int k = 0; k < kBK / kUmmaK; ++k)
+                        mma_i8_cg2(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdescPair, (kb | k) != 0 ? 1u : 0u);
+                    mma_commit_pair(&empty[stage]);
+                    if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
+                }
+                mma_commit_pair(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+            }
+        }
+    } else {
+        // ---------------- epilogue (both CTAs: their own 128 rows)
+        const int quarter = warp & 3;
+        const int row_in_tile = quarter * 32 + lane;
+        const uint32_t tempty_leader0 = mapa_u32(&tempty[0], 0);
+        const uint32_t tempty_leader1 = mapa_u32(&tempty[1], 0);
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+            const int64_t m0 = (tile / num_n_tiles) * (2 * kBM) + rank * kBM;
+            const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
+            const int64_t row = m0 + row_in_tile;
+            const bool row_ok = row < K;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            int32_t partial = 0;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                   static_cast<uint32_t>(acc * kBN);
+#pragma unroll 1
+            for (int c = 0; c < kBN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
+                tmem_wait_ld();
+                const int col0 = n0 + c * 32;
+                uint32_t bits = 0;
+                if (row_ok && (col0 >> 6) < W64)
+                    bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
+                if constexpr (SYM) {
+                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const int4 d = __ldg(dg + i4);
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = 4 * i4 + e;
+                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
+                }
+                if (!SYM && emit_gains && row_ok && col0 < n_pad) {
+                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+                    int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
+#pragma unroll
+                    for (int i4 = 0; i4 < 8; ++i4) {
+                        const int4 d = __ldg(dg + i4);
+                        int o[4];
+                        const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = 4 * i4 + e;
+                            const int y2 = 2 * static_cast<int32_t>(v[i]);
+                            o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
+                        }
+                        __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+            if (row_ok)
+                atomicAdd(reinterpret_cast<unsigned long long *>(f + row),
+                          static_cast<unsigned long long>(static_cast<int64_t>(partial)));
+            if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();                           // all MMAs retired, both epilogues done
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg2(tmem_base, kTmemCols);
+    }
+}
+
+bool g_pair_attr_set = false;
+
 // ---------------------------------------------------------------- batch statistics
 __global__ void __launch_bounds__(1024) stats_kernel(const int64_t *__restrict__ f, int64_t K,
                                                      int rank, int world,
@@ -241,8 +426,8 @@ bool g_attr_set = false;
 
 }  // namespace
 
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q, int64_t *f_out,
-                    bool sym) {
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane, int64_t *f_out, bool sym) {
+    const CUtensorMap *tmap_q = plane >= 0 ? &c.tmap_Qs[plane] : nullptr;
     if (k <= 0) return;
     if (!g_attr_set) {
         cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -253,10 +438,33 @@ void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_
     }
     const int num_n_tiles = (c.n + kBN - 1) / kBN;
     const int num_k_blocks = c.n_pad / kBK;
+    const bool use_sym = sym && !emit_gains;
+    if (c.eval_pair) {
+        if (!g_pair_attr_set) {
+            cudaFuncSetAttribute(eval_tc_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kPairSmemBytes));
+            cudaFuncSetAttribute(eval_tc_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kPairSmemBytes));
+            g_pair_attr_set = true;
+        }
+        const int64_t num_tiles = ((k + 2 * kBM - 1) / (2 * kBM)) * num_n_tiles;
+        const int64_t pairs = num_tiles < c.num_sms / 2 ? num_tiles : c.num_sms / 2;
+        const CUtensorMap &tq = use_sym ? c.tmap_Q8L_h : (plane >= 0 ? c.tmap_Qs_h[plane] : c.tmap_Q8_h);
+        if (use_sym)
+            eval_tc_pair_kernel<true><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
+                c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
+                f_out ? f_out : c.f, nullptr, 0);
+        else
+            eval_tc_pair_kernel<false><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
+                c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
+                f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+        ++c.launches;
+        return;
+    }
     const int64_t num_m_tiles = (k + kBM - 1) / kBM;
     const int64_t num_tiles = num_m_tiles * num_n_tiles;
     const int grid = static_cast<int>(num_tiles < c.num_sms ? num_tiles : c.num_sms);
-    if (sym && !emit_gains)
+    if (use_sym)
         eval_tc_kernel<true><<<grid, kThreads, kSmemBytes, c.stream>>>(
             c.tmap_X8, c.tmap_Q8L, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb,
             c.diag, f_out ? f_out : c.f, nullptr, 0);

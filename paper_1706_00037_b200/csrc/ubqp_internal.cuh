@@ -54,6 +54,10 @@ struct Ctx {
     CUtensorMap tmap_X8{}, tmap_Q8{};
     int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
     CUtensorMap tmap_Q8L{};
+    // 128-row B boxes for the CTA-pair (cta_group::2) evaluation: each CTA loads half of N
+    CUtensorMap tmap_Q8_h{}, tmap_Q8L_h{};
+    CUtensorMap tmap_Qs_h[kSlices]{};
+    bool eval_pair = true;       // UBQP_EVAL_2SM=0 selects the single-CTA kernel
     bool sym_eval = true;        // f-only evaluations use the triangular GEMM (UBQP_FULL_EVAL disables)
     // real-valued Q (a4'): Q~ = 2^-q_exp * sum_s 128^s L_s, int8 limb planes L_s in [-64, 63]
     bool real = false;
@@ -74,8 +78,9 @@ void launch_random(Ctx &c, uint64_t seed, int64_t k);
 void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
 void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer or real planes
 // eval_tc.cu
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, const CUtensorMap *tmap_q = nullptr,
-                    int64_t *f_out = nullptr, bool sym = false);
+// plane = -1: the integer Q8; plane >= 0: limb plane of a real-valued Q
+void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane = -1, int64_t *f_out = nullptr,
+                    bool sym = false);
 void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev);
 void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
 // screen.cu
@@ -207,6 +212,60 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
           "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
           "=r"(v[31])
         : "r"(taddr));
+}
+
+// ---- CTA pair (cluster of 2, cta_group::2)
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void *p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_cg2(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+                 "r"(ncols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_cg2(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
+}
+// each CTA of the pair loads its half into its own smem; bytes complete on the leader's barrier
+__device__ __forceinline__ void tma_load_2d_cg2(void *dst, const CUtensorMap *m, int x, int y,
+                                                uint32_t leader_bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(leader_bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void mma_i8_cg2(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// arrive (when the issued MMAs retire) on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
 }
 
 // UMMA shared-memory descriptor: K-major operand, 128-byte swizzle, rows of 128 B,
