@@ -313,17 +313,25 @@ def test_multistart_rounds_match_oracle(n, K, rounds, lam):
 @pytest.mark.parametrize("n", [1, 2, 200, 257, 513, 2500])
 def test_symmetric_and_full_eval_agree(n, monkeypatch):
     """f-only evaluations use the triangular GEMM (NEXT-1); UBQP_FULL_EVAL=1 forces the full
-    one.  Both must equal the oracle exactly."""
+    one; UBQP_EVAL_2SM=0 the single-CTA kernel.  All must equal the oracle exactly."""
     Q = generate_Q(n, 0.6, seed=n + 40)
     K = 300
     X = oracle.random_solutions(n, 21, K)
     ref = oracle.eval_batch(Q, X, nthreads=8)
-    for full in ("0", "1"):
-        monkeypatch.setenv("UBQP_FULL_EVAL", full)
-        u = _handle_with(Q, K)
-        u.random(21, K)
-        f = np.zeros(K, np.int64)
-        st = ubqp_stats()
-        u.eval_batch(0, f, st)
-        assert np.array_equal(f, ref), full
-        assert st.max_key == oracle.stats(ref)[2]
+    for pair in ("1", "0"):                       # CTA-pair (cta_group::2) and single-CTA kernels
+        monkeypatch.setenv("UBQP_EVAL_2SM", pair)
+        for full in ("0", "1"):
+            monkeypatch.setenv("UBQP_FULL_EVAL", full)
+            u = _handle_with(Q, K)
+            u.random(21, K)
+            f = np.zeros(K, np.int64)
+            st = ubqp_stats()
+            u.eval_batch(0, f, st)
+            assert np.array_equal(f, ref), (pair, full)
+            assert st.max_key == oracle.stats(ref)[2]
+            if n <= 513:
+                u.eval_batch(UBQP_EMIT_GAINS, f)
+                G = np.zeros((K, n), np.int32)
+                u.get_gains(0, K, G)
+                for k in (0, K // 2, K - 1):
+                    assert np.array_equal(G[k].astype(np.int64), oracle.gains(Q, X[k])), (pair, k)
