@@ -177,6 +177,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     build_lib()
     torch.cuda.set_device(local_rank)
+    backend = os.environ.get("UBQP_DIST_BACKEND", "nccl")
     peaks = load_peaks()
     n, K, lam = cfg["n"], cfg["K"], cfg["lam"]
     Q = generate_Q(n, cfg["density"], seed=cfg["seed_Q"])
@@ -306,8 +307,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         except Exception:
             traffic = {}
     roof_eval = {"bound": "tensor", "achieved": eval_tops, "peak": int8_peak, "unit": "TOP/s",
-                 "frac": eval_tops / int8_peak, "traffic": traffic.get("eval_tc_kernel"),
-                 "kernel": "eval_tc_kernel (+stats)", "ms": eval_ms,
+                 "frac": eval_tops / int8_peak,
+                 "traffic": traffic.get("eval_tc_pair_kernel", traffic.get("eval_tc_kernel")),
+                 "kernel": "eval_tc_pair_kernel (+stats)", "ms": eval_ms,
                  "peak_note": ("measured cuBLASLt int8 GEMM (torch._int_mm 8192^3, best of 10) on this GPU"
                                if int8_meas else "int8 = 2 x bf16 " + peaks["_source"]),
                  "int8_measured": int8_meas,
@@ -322,8 +324,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int8xint8->int32 eval, int32/int64 ascent", "data": "synthetic",
-        "config": workload_config(cfg, world),
+        "vs_baseline": None, "dtype": "int8", "data": "synthetic",
+        "dtype_detail": "int8 x int8 -> int32 tensor-core eval, int32 gains / int64 f in the ascent",
+        "config": workload_config(cfg, world, {"dist_backend": backend if world > 1 else None}),
         "roofline": dominant,
         "roofline_eval": roof_eval, "roofline_ascent": roof_asc,
         "eval_only_evals_per_s": K / (eval_ms * 1e-3),
@@ -341,6 +344,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["table1_eval_1000"] = table1_eval(local_rank)
         out["real_q_eval"] = real_q_eval(local_rank)
         out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
+        out["ascent_microbench"] = ascent_microbench(local_rank)
     print(json.dumps(out), flush=True)
 
 
@@ -448,6 +452,37 @@ def f_only_eval(device, cfg, Q):
             "note": "n(n+1) ops per evaluation (upper triangle incl. diagonal)"}
 
 
+def ascent_microbench(device):
+    """SURVEY §8(d) microbench A: m = 8192 random starts (SplitMix64 seed 5), dense n in
+    {2500, 5000, 7000}, full steepest ascent (max_flips = 10n): flip steps/s."""
+    import torch
+
+    from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp
+    out = {}
+    m = 8192
+    for n in (2500, 5000, 7000):
+        Q = generate_Q(n, 1.0, seed=5)
+        u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+        u.load_Q(Q, m)
+        u.random(5, m)
+        u.eval_batch(UBQP_EMIT_GAINS)
+        slots = torch.arange(m, dtype=torch.int32, device="cuda")
+        flips = torch.zeros(m, dtype=torch.int32, device="cuda")
+        fo = torch.zeros(m, dtype=torch.int64, device="cuda")
+        u.ascend(slots, m, 10 * n, fo, flips)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u.ascend(slots, m, 10 * n, fo, flips)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        steps = int(flips.sum().item())
+        out[f"n{n}"] = {"ms": ms, "flip_steps": steps, "steps_per_s": steps / (ms * 1e-3),
+                        "TB_per_s_qrow": steps * n / (ms * 1e-3) / 1e12}
+        u.close()
+    return out
+
+
 def real_q_eval(device):
     """a4': real-valued Q (n = 7000 dense, U(-100,100) float32), 65536 random solutions:
     four int8 limb-plane evaluations + exact combine."""
@@ -497,11 +532,18 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
+    # UBQP_DIST_BACKEND=gloo + fewer GPUs than ranks: a functional check of the multi-rank path
+    # on one GPU (ranks share a device; only host-side collectives, no kernel waits on a peer).
+    backend = os.environ.get("UBQP_DIST_BACKEND", "nccl")
     if world > 1:
         import torch
         import torch.distributed as dist
+        local_rank = local_rank % torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:
