@@ -283,7 +283,7 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
     const bool full = 16 * BLOCK * NCH <= c.q_ld;
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
     // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
-    constexpr int kRegs = NCH >= 6 ? 256 : 24 * NCH + 48;
+    constexpr int kRegs = NCH >= 5 ? 170 : 24 * NCH + 48;   // 170: 6 CTAs of 64 threads per SM (small spills at NCH = 7, measured faster)
     constexpr int kMinBlocks = (65536 / (BLOCK * kRegs)) < 1 ? 1 : 65536 / (BLOCK * kRegs);
     if (full)
         ascend_kernel<BLOCK, NCH, kMinBlocks, true><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
