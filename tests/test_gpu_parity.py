@@ -258,9 +258,10 @@ def test_full_size_sampled(n, K, kind):
     assert st.sum == int(f.sum()) and st.count == K
 
 
-@pytest.mark.parametrize("n", [5000, 7000])
+@pytest.mark.parametrize("n", [5000, 7000, 9000, 12000])
 def test_ascend_full_size(n):
-    """The bench shapes (64x7 at n = 5000 and n = 7000), exact against the oracle."""
+    """Default shapes 64x5 (n=5000), 64x7 (n=7000), 96x6 (n=9000), 128x6 (n=12000), exact
+    against the oracle."""
     Q = generate_Q(n, 1.0, seed=4)
     K = 24
     u = _handle_with(Q, K)
