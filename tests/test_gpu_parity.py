@@ -336,3 +336,49 @@ def test_symmetric_and_full_eval_agree(n, monkeypatch):
                 u.get_gains(0, K, G)
                 for k in (0, K // 2, K - 1):
                     assert np.array_equal(G[k].astype(np.int64), oracle.gains(Q, X[k])), (pair, k)
+
+
+def test_bench_round_full_size():
+    """The exact bench step (config 4: n = 7000, K = 262144 Glover, lambda = 0.5, max_flips =
+    10n): sampled survivors are ascended by the oracle and compared exactly; for ALL survivors
+    the outputs are checked by properties at full size: f equals an independent re-evaluation
+    of the returned bits, and every returned solution is a 1-flip local optimum (all gains
+    <= 0, recomputed by the eval kernel) unless it used max_flips."""
+    from paper_1706_00037_b200.multistart import MultiStart
+    from inputs import CONFIGS
+    cfg = CONFIGS[4]
+    n, K = cfg["n"], cfg["K"]
+    Q = generate_Q(n, cfg["density"], seed=cfg["seed_Q"])
+    ms = MultiStart(Q, K, lam=cfg["lam"], max_flips=cfg["max_flips"])
+    x0_bits, f0 = ms.first_derivative()
+    res = ms.round(x0_bits, 0, f0)
+    m = res.m
+    assert m > 1000
+    surv = ms.surv[:m].cpu().numpy()
+    f_asc = ms.f_asc[:m].cpu().numpy()
+    flips = ms.flips[:m].cpu().numpy()
+    bits = ms.bits[:m].cpu().numpy().view(np.uint64)
+    # sampled exact comparison with the oracle
+    x0 = unpack_bits(x0_bits.cpu().numpy().view(np.uint64), n)[0]
+    rng = np.random.default_rng(3)
+    pick = np.unique(np.concatenate([[0, m - 1], rng.integers(0, m, 10)]))
+    X0 = np.stack([oracle.diversify(x0, int(surv[i]), 1)[0] for i in pick])
+    Xr, fr, flr = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0, nthreads=8), cfg["max_flips"], nthreads=8)
+    assert np.array_equal(f_asc[pick], fr) and np.array_equal(flips[pick], flr)
+    assert np.array_equal(unpack_bits(bits[pick], n), Xr)
+    # full-size properties through an independent evaluation of the returned solutions
+    u = _handle_with(Q, m)
+    u.set_batch(bits.copy(), m)
+    f_re = torch.zeros(m, dtype=torch.int64, device="cuda")
+    u.eval_batch(UBQP_EMIT_GAINS, f_re)
+    torch.cuda.synchronize()
+    assert np.array_equal(f_re.cpu().numpy(), f_asc)
+    chunk = 16384
+    G = torch.empty((chunk, n), dtype=torch.int32, device="cuda")
+    for s0 in range(0, m, chunk):
+        c = min(chunk, m - s0)
+        u.get_gains(s0, c, G[:c])
+        torch.cuda.synchronize()
+        gmax = G[:c].max(dim=1).values.cpu().numpy()
+        capped = flips[s0:s0 + c] >= cfg["max_flips"]
+        assert np.all((gmax <= 0) | capped)
