@@ -209,12 +209,31 @@ constexpr uint32_t kPairStageBytes = 2 * kABytes;                    // 16 KB A 
 constexpr size_t kPairSmemBytes = static_cast<size_t>(kPairStages) * kPairStageBytes + 1024 + 256;
 constexpr uint32_t kIdescPair = dev::idesc_i8(2 * kBM, kBN);
 
+// Work item = (M tile of 256 rows, N tile of 256 columns, K split).  f-only launches with
+// fewer tiles than CTA pairs split K (f is linear in Y, so the partial row-dots of the splits
+// add up in the int64 atomics; the -Q_jj term of SYM goes with split 0).
+struct PairTile {
+    int mt, nt, kb0, kb1;
+};
+template <bool SYM>
+__device__ __forceinline__ PairTile pair_tile(int64_t tile, int num_n_tiles, int num_k_blocks, int ksplit) {
+    PairTile t;
+    const int64_t mn = tile / ksplit;
+    const int ks = static_cast<int>(tile - mn * ksplit);
+    t.mt = static_cast<int>(mn / num_n_tiles);
+    t.nt = static_cast<int>(mn - static_cast<int64_t>(t.mt) * num_n_tiles);
+    const int kbs = SYM ? min(num_k_blocks, (t.nt + 1) * (kBN / kBK)) : num_k_blocks;
+    t.kb0 = ks * kbs / ksplit;
+    t.kb1 = (ks + 1) * kbs / ksplit;
+    return t;
+}
+
 template <bool SYM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQh,
                     int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
                     const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
-                    int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains) {
+                    int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains, int ksplit) {
     using namespace dev;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -260,11 +279,11 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
-                const int m0 = static_cast<int>(tile / num_n_tiles) * (2 * kBM) + static_cast<int>(rank) * kBM;
-                const int nt = static_cast<int>(tile % num_n_tiles);
-                const int n0 = nt * kBN + static_cast<int>(rank) * (kBN / 2);
-                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
-                for (int kb = 0; kb < kbs; ++kb) {
+                const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
+                if (pt.kb0 == pt.kb1) continue;
+                const int m0 = pt.mt * (2 * kBM) + static_cast<int>(rank) * kBM;
+                const int n0 = pt.nt * kBN + static_cast<int>(rank) * (kBN / 2);
+                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
                     const uint32_t fb = mapa_u32(&full[stage], 0);
@@ -282,19 +301,20 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
+                const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
+                if (pt.kb0 == pt.kb1) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1u);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
-                const int nt = static_cast<int>(tile % num_n_tiles);
-                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
-                for (int kb = 0; kb < kbs; ++kb) {
+                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
                     const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kABytes));
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k)
-                        mma_i8_cg2(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdescPair, (kb | k) != 0 ? 1u : 0u);
+                        mma_i8_cg2(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdescPair,
+                                   (kb != pt.kb0 || k != 0) ? 1u : 0u);
                     mma_commit_pair(&empty[stage]);
                     if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
                 }
@@ -311,8 +331,11 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
-            const int64_t m0 = (tile / num_n_tiles) * (2 * kBM) + rank * kBM;
-            const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
+            const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
+            if (pt.kb0 == pt.kb1) continue;
+            const bool with_diag = pt.kb0 == 0;
+            const int64_t m0 = static_cast<int64_t>(pt.mt) * (2 * kBM) + rank * kBM;
+            const int n0 = pt.nt * kBN;
             const int64_t row = m0 + row_in_tile;
             const bool row_ok = row < K;
             mbar_wait(&tfull[acc], acc_phase);
@@ -338,7 +361,7 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             const int i = 4 * i4 + e;
-                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
+                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - (with_diag ? dd[e] : 0) : 0;
                         }
                     }
                 } else {
@@ -447,17 +470,22 @@ void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane, int64_t *f_ou
                                  static_cast<int>(kPairSmemBytes));
             g_pair_attr_set = true;
         }
-        const int64_t num_tiles = ((k + 2 * kBM - 1) / (2 * kBM)) * num_n_tiles;
+        const int64_t mn_tiles = ((k + 2 * kBM - 1) / (2 * kBM)) * num_n_tiles;
+        // f-only launches too small to fill the pairs twice split K (<= 8 ways)
+        int ksplit = 1;
+        if (!emit_gains)
+            while (ksplit < 8 && mn_tiles * ksplit < c.num_sms && num_k_blocks >= 4 * ksplit) ksplit *= 2;
+        const int64_t num_tiles = mn_tiles * ksplit;
         const int64_t pairs = num_tiles < c.num_sms / 2 ? num_tiles : c.num_sms / 2;
         const CUtensorMap &tq = use_sym ? c.tmap_Q8L_h : (plane >= 0 ? c.tmap_Qs_h[plane] : c.tmap_Q8_h);
         if (use_sym)
             eval_tc_pair_kernel<true><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
                 c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
-                f_out ? f_out : c.f, nullptr, 0);
+                f_out ? f_out : c.f, nullptr, 0, ksplit);
         else
             eval_tc_pair_kernel<false><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
                 c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
-                f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
+                f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0, ksplit);
         ++c.launches;
         return;
     }
