@@ -28,6 +28,63 @@ constexpr uint32_t kTmemCols = 2 * kBN;             // two 128 x 256 s32 accumul
 constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
 constexpr uint32_t kIdesc = dev::idesc_i8(kBM, kBN);
 
+// Epilogue of one 128-row x 256-column accumulator (thread = row): drains TMEM 32 columns at a
+// time and folds  f_k += sum_j x_kj Y_kj  (or, triangular: x_kj (2 Y_kj - Q_jj), the Q_jj term
+// only in the K split that owns the diagonal) and, with gains, stores
+// Delta_kj = Q_jj + 2 (1 - 2 x_kj) Y_kj.  Returns the row's int32 partial of f.
+template <bool SYM>
+__device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bool row_ok, int n0, int W64,
+                                                 int n_pad, const uint64_t *__restrict__ Xb,
+                                                 const int32_t *__restrict__ diag, int32_t *__restrict__ gains,
+                                                 int emit_gains, bool with_diag) {
+    using namespace dev;
+    int32_t partial = 0;
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
+        tmem_wait_ld();
+        const int col0 = n0 + c * 32;
+        uint32_t bits = 0;
+        if (row_ok && (col0 >> 6) < W64)
+            bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
+        if constexpr (SYM) {
+            const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+#pragma unroll
+            for (int i4 = 0; i4 < 8; ++i4) {
+                const int4 d = __ldg(dg + i4);
+                const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = 4 * i4 + e;
+                    partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - (with_diag ? dd[e] : 0) : 0;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
+            if (emit_gains && row_ok && col0 < n_pad) {
+                const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+                int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
+#pragma unroll
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const int4 d = __ldg(dg + i4);
+                    int o[4];
+                    const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int i = 4 * i4 + e;
+                        const int y2 = 2 * static_cast<int32_t>(v[i]);
+                        o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
+                    }
+                    __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));   // streaming: keep X/Q in L2
+                }
+            }
+        }
+    }
+    return partial;
+}
+
 // SYM (f only, NEXT-1 of SURVEY §8(f)): B = the lower triangle of Q (row j keeps Q_ji, i <= j),
 // so tile column block J needs only K blocks covering rows i < 256(J+1): ~(n+256)/(2n) of the
 // MMAs.  f = sum_j x_j (2 Y^U_j - Q_jj) with Y^U_j = sum_{i<=j} x_i Q_ij  (Q = Q^t).
@@ -136,53 +193,9 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             const bool row_ok = row < K;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            int32_t partial = 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                   static_cast<uint32_t>(acc * kBN);
-#pragma unroll 1
-            for (int c = 0; c < kBN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
-                tmem_wait_ld();
-                const int col0 = n0 + c * 32;
-                uint32_t bits = 0;
-                if (row_ok && (col0 >> 6) < W64)
-                    bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
-                if constexpr (SYM) {
-                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int4 d = __ldg(dg + i4);
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int i = 4 * i4 + e;
-                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
-                }
-                if (!SYM && emit_gains && row_ok && col0 < n_pad) {
-                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
-                    int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int4 d = __ldg(dg + i4);
-                        int o[4];
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int i = 4 * i4 + e;
-                            const int y2 = 2 * static_cast<int32_t>(v[i]);
-                            o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
-                        }
-                        __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));   // streaming: keep X/Q in L2
-                    }
-                }
-            }
+            const int32_t partial = epilogue_tile<SYM>(
+                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN),
+                row, row_ok, n0, W64, n_pad, Xb, diag, gains, emit_gains, true);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             if (row_ok)
@@ -340,53 +353,9 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             const bool row_ok = row < K;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            int32_t partial = 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                                   static_cast<uint32_t>(acc * kBN);
-#pragma unroll 1
-            for (int c = 0; c < kBN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
-                tmem_wait_ld();
-                const int col0 = n0 + c * 32;
-                uint32_t bits = 0;
-                if (row_ok && (col0 >> 6) < W64)
-                    bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
-                if constexpr (SYM) {
-                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int4 d = __ldg(dg + i4);
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int i = 4 * i4 + e;
-                            partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - (with_diag ? dd[e] : 0) : 0;
-                        }
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
-                }
-                if (!SYM && emit_gains && row_ok && col0 < n_pad) {
-                    const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
-                    int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
-#pragma unroll
-                    for (int i4 = 0; i4 < 8; ++i4) {
-                        const int4 d = __ldg(dg + i4);
-                        int o[4];
-                        const int dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const int i = 4 * i4 + e;
-                            const int y2 = 2 * static_cast<int32_t>(v[i]);
-                            o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
-                        }
-                        __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));
-                    }
-                }
-            }
+            const int32_t partial = epilogue_tile<SYM>(
+                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN),
+                row, row_ok, n0, W64, n_pad, Xb, diag, gains, emit_gains, with_diag);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
