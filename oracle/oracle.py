@@ -203,6 +203,10 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
     mean_count = K
     inc_x = first_derivative_start(Q)
     inc_f = xQx(Q, inc_x)
+    if lam == "paper":
+        # P:55 lambda = Max/Mean = Starting_solution/Mean; SPEC S:244 clamp to (0, 1], 0.5 fallback
+        m = mean_sum / mean_count
+        lam = 0.5 if (m <= 0 or inc_f <= 0) else min(1.0, max(1e-6, inc_f / m))
     traj = [(0, inc_f)]
     for rnd in range(1, rounds + 1):
         t0 = (rnd - 1) * K

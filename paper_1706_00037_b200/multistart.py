@@ -33,6 +33,14 @@ def key_g(key: int) -> int:
     return (1 << KEY_SHIFT) - 1 - (int(key) & ((1 << KEY_SHIFT) - 1))
 
 
+def paper_lambda(mean: float, start_value: int) -> float:
+    """P:55 "lambda is initially set to Max / Mean = Starting_solution / Mean", clamped to
+    (0, 1]: the raw ratio exceeds 1 whenever the start beats the mean (R7)."""
+    if mean <= 0 or start_value <= 0:
+        return 0.5
+    return min(1.0, max(1e-6, start_value / mean))
+
+
 def dist_info(group=None):
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(group), dist.get_world_size(group)
@@ -159,11 +167,15 @@ class MultiStart:
             best_bits = self.bits[i].clone()
         return RoundResult(m, T, best_key, best_bits, batch_max, mean_sum, mean_count)
 
-    def run(self, rounds: int, sample_seed: int, t_start: int = 0):
+    def run(self, rounds: int, sample_seed: int, t_start: int = 0, lam_policy: str = "fixed"):
         """Figure 2 as batched rounds (O8): pinned sampling mean, first-derivative
-        incumbent, rounds of diversify/eval/screen/ascend; strict improvement."""
+        incumbent, rounds of diversify/eval/screen/ascend; strict improvement.
+        lam_policy "paper": lambda = Max/Mean = Starting_solution/Mean, clamped to
+        (0, 1] with 0.5 when Mean <= 0 or the start's value <= 0 (R7)."""
         mean = self.sample_mean(sample_seed)
         inc_bits, inc_f = self.first_derivative()
+        if lam_policy == "paper":
+            self.lam = paper_lambda(mean[0] / mean[1], inc_f)
         traj = [(0, inc_f)]
         for r in range(1, rounds + 1):
             res = self.round(inc_bits, t_start + (r - 1) * self.K, inc_f, mean)

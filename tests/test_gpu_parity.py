@@ -382,3 +382,13 @@ def test_bench_round_full_size():
         gmax = G[:c].max(dim=1).values.cpu().numpy()
         capped = flips[s0:s0 + c] >= cfg["max_flips"]
         assert np.all((gmax <= 0) | capped)
+
+
+def test_multistart_paper_lambda_matches_oracle():
+    from paper_1706_00037_b200.multistart import MultiStart
+    n, K = 200, 1500
+    Q = generate_Q(n, 0.5, seed=77)
+    ms = MultiStart(Q, K, lam=0.5, max_flips=10 * n)
+    best, bits, traj = ms.run(3, sample_seed=9, lam_policy="paper")
+    obest, ox, otraj = oracle.run_rounds(Q, K, 3, "paper", 10 * n, sample_seed=9, nthreads=8)
+    assert best == obest and traj == otraj

@@ -374,3 +374,12 @@ def test_real_oracle_closed_forms_and_exact_rounding():
     S = np.flatnonzero(x)
     exact = sum(Fraction(float(v)) for v in Q[np.ix_(S, S)].ravel())
     assert oracle.xQx_real(Q, x) == float(exact)
+
+
+def test_paper_lambda_policy_spec_examples():
+    """(mean 100, start 200) -> 1.0; (mean -0.5, start 2) -> 0.5; (100, 100) -> 1.0."""
+    from paper_1706_00037_b200.multistart import paper_lambda
+    assert paper_lambda(100.0, 200) == 1.0
+    assert paper_lambda(-0.5, 2) == 0.5
+    assert paper_lambda(100.0, 100) == 1.0
+    assert paper_lambda(400.0, 100) == 0.25
