@@ -22,6 +22,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
     "-cudart", "static",
     "--expt-relaxed-constexpr",
+    "--split-compile=0",
 ]
 
 
