@@ -149,7 +149,9 @@ int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count,
  * Delta.  Outputs per i: f_out int64[m], flips_out int32[m], bits_out uint64[m][W64]
  * (any may be NULL), best_key_out: one int64 = max over i of max_key(f_i, g(s_i))
  * (-1 if m == 0; may be NULL).  The batch itself is not modified.
- * Errors: E_INVALID (slot out of range, m > k_local, max_flips < 0), E_STATE. */
+ * Errors: E_INVALID (slot out of range, m > k_local, max_flips < 0), E_STATE.  Host slots are
+ * range-checked before launch; device-resident slots are checked in the kernel, and an
+ * out-of-range one yields flips_out[i] = -1 (E_INVALID when flips_out is a host array). */
 int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
                 int64_t *f_out, int32_t *flips_out, uint64_t *bits_out,
                 int64_t *best_key_out);

@@ -374,7 +374,6 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     }
 }
 
-bool g_pair_attr_set = false;
 
 // ---------------------------------------------------------------- batch statistics
 __global__ void __launch_bounds__(1024) stats_kernel(const int64_t *__restrict__ f, int64_t K,
@@ -414,30 +413,29 @@ __global__ void __launch_bounds__(1024) stats_kernel(const int64_t *__restrict__
     }
 }
 
-bool g_attr_set = false;
 
 }  // namespace
 
 void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane, int64_t *f_out, bool sym) {
     const CUtensorMap *tmap_q = plane >= 0 ? &c.tmap_Qs[plane] : nullptr;
     if (k <= 0) return;
-    if (!g_attr_set) {
+    if (!c.eval_attr_set) {   // per handle (= per device): the attribute is per device context
         cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes));
         cudaFuncSetAttribute(eval_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(kSmemBytes));
-        g_attr_set = true;
+        c.eval_attr_set = true;
     }
     const int num_n_tiles = (c.n + kBN - 1) / kBN;
     const int num_k_blocks = c.n_pad / kBK;
     const bool use_sym = sym && !emit_gains;
     if (c.eval_pair) {
-        if (!g_pair_attr_set) {
+        if (!c.eval_pair_attr_set) {
             cudaFuncSetAttribute(eval_tc_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kPairSmemBytes));
             cudaFuncSetAttribute(eval_tc_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kPairSmemBytes));
-            g_pair_attr_set = true;
+            c.eval_pair_attr_set = true;
         }
         const int64_t mn_tiles = ((k + 2 * kBM - 1) / (2 * kBM)) * num_n_tiles;
         // f-only launches too small to fill the pairs twice split K (<= 8 ways)

@@ -58,6 +58,7 @@ struct Ctx {
     CUtensorMap tmap_Q8_h{}, tmap_Q8L_h{};
     CUtensorMap tmap_Qs_h[kSlices]{};
     bool eval_pair = true;       // UBQP_EVAL_2SM=0 selects the single-CTA kernel
+    bool eval_attr_set = false, eval_pair_attr_set = false;   // dynamic-smem opt-in done
     bool sym_eval = true;        // f-only evaluations use the triangular GEMM (UBQP_FULL_EVAL disables)
     // real-valued Q (a4'): Q~ = 2^-q_exp * sum_s 128^s L_s, int8 limb planes L_s in [-64, 63]
     bool real = false;
