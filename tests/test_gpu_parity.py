@@ -392,3 +392,36 @@ def test_multistart_paper_lambda_matches_oracle():
     best, bits, traj = ms.run(3, sample_seed=9, lam_policy="paper")
     obest, ox, otraj = oracle.run_rounds(Q, K, 3, "paper", 10 * n, sample_seed=9, nthreads=8)
     assert best == obest and traj == otraj
+
+
+@pytest.mark.parametrize("n", [16384])
+def test_limits_max_n_and_coefficients(n):
+    """The documented limits: n = 16384 (largest ascent shape 160x7) with every coefficient
+    at +127 or -127, where |Y| = n*127, |Delta| = (2n-1)*127 (keys 256*Delta ~ 1.07e9, next to
+    the int32 edge) and f = 127 n^2 exercise every overflow bound of include/ubqp.h."""
+    rng = np.random.default_rng(5)
+    sign = np.where(rng.random((n, n)) < 0.5, -1, 1).astype(np.int32)
+    Q = 127 * np.triu(sign)
+    Q = Q + np.triu(Q, 1).T                                  # symmetric, all entries +-127
+    Qp = np.full((n, n), 127, dtype=np.int32)               # all +127: ascent from 0 flips everything
+    for QQ, name in ((Qp, "plus"), (Q, "mixed")):
+        u = _handle_with(QQ, 4)
+        X = np.zeros((4, n), np.uint8)
+        X[1] = 1
+        X[2:] = rng.integers(0, 2, size=(2, n))
+        u.set_batch(pack_bits(X), 4)
+        f = np.zeros(4, np.int64)
+        u.eval_batch(UBQP_EMIT_GAINS, f)
+        fo = oracle.eval_batch(QQ, X, nthreads=8)
+        assert np.array_equal(f, fo), name
+        if name == "plus":
+            assert f[1] == 127 * n * n
+        slots = np.array([0, 2], np.int32)
+        fa = np.zeros(2, np.int64)
+        fl = np.zeros(2, np.int32)
+        ba = np.zeros((2, u.W64), np.uint64)
+        u.ascend(slots, 2, 10 * n, fa, fl, ba)
+        Xr, fr, flr = oracle.ascend(QQ, X[slots], fo[slots], 10 * n, nthreads=2)
+        assert np.array_equal(fa, fr) and np.array_equal(fl, flr), name
+        assert np.array_equal(unpack_bits(ba, n), Xr), name
+        u.close()
