@@ -20,7 +20,7 @@ _lib = None
 
 __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
-    "glover_params", "diversify", "max_key", "stats", "threshold", "screen", "ascend",
+    "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
     "first_derivative_start", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
 ]
 
@@ -51,6 +51,7 @@ def _L():
         lib.oracle_random.argtypes = [i32, u64, i64, i32, i32, P]
         lib.oracle_glover_params.argtypes = [i64, i32, P, P, P]
         lib.oracle_diversify.argtypes = [i32, P, i64, i64, i32, i32, P]
+        lib.oracle_blend.argtypes = [i32, P, P, i64, i64, i64, i32, i32, P]
         lib.oracle_max_key.argtypes = [i64, i64]
         lib.oracle_max_key.restype = i64
         lib.oracle_stats.argtypes = [i64, P, i32, i32, P]
@@ -135,6 +136,33 @@ def diversify(seed_x, t0: int, k_local: int, rank: int = 0, world: int = 1) -> n
     return X
 
 
+# O4b -- blend of the incumbent with parent g mod P on the Glover mask (R11b)
+def blend(seed_x, parents, t0: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+    seed_x = np.ascontiguousarray(seed_x, dtype=np.uint8).reshape(-1)
+    n = seed_x.shape[0]
+    parents = np.ascontiguousarray(parents, dtype=np.uint8).reshape(-1, n)
+    if parents.shape[0] < 1:
+        raise ValueError("blend needs at least one parent")
+    X = np.zeros((k_local, n), dtype=np.uint8)
+    _L().oracle_blend(n, _p(seed_x), _p(parents), parents.shape[0], t0, k_local, rank, world, _p(X))
+    return X
+
+
+def pool_update(pool: list, pool_cap: int, inc_x, improved_from, round_best):
+    """Parent pool of the blend policy (R11b): distinct local optima other than the
+    incumbent, oldest first, at most pool_cap.  After a round, the replaced incumbent
+    (improved_from) or else the round's best ascended solution joins the pool unless it
+    equals the incumbent or is already pooled."""
+    cand = improved_from if improved_from is not None else round_best
+    if cand is None:
+        return pool
+    cand = np.asarray(cand, dtype=np.uint8)
+    if np.array_equal(cand, inc_x) or any(np.array_equal(cand, p) for p in pool):
+        return pool
+    pool = pool + [cand.copy()]
+    return pool[-pool_cap:]
+
+
 # O5 -- stats {sum, count, max_key} (P:49, P:91; R14)
 def max_key(f: int, g: int) -> int:
     return int(_L().oracle_max_key(f, g))
@@ -182,7 +210,7 @@ def first_derivative_start(Q) -> np.ndarray:
 
 # O8 -- batched rounds of Figure 2 (R5, R6, R13)
 def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
-               world: int = 1, nthreads: int = 1):
+               world: int = 1, nthreads: int = 1, div: str = "glover", pool_cap: int = 8):
     """Round 0: K random starts (O3, seed ``sample_seed``) -> pinned (mean_sum, mean_count)
     (P:55 "the mean is the average xQx value derived during sampling").  Incumbent =
     first-derivative start.  Round r >= 1: diversify from the incumbent with
@@ -190,6 +218,8 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
     batch max) (R6), screen, ascend survivors, replace the incumbent iff the
     best ascended f is strictly greater, ties -> lowest g (R8, R14).
     ``world`` shards every batch cyclically (O10); results must not depend on it.
+    ``div`` "blend": once the parent pool (pool_update) is non-empty, rounds blend the
+    incumbent with pool[g mod P] (O4b) instead of O4.
     Returns (best_value, best_x, trajectory[list of (round, best_value)])."""
     Q = _Q(Q)
     n = Q.shape[0]
@@ -208,10 +238,15 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
         m = mean_sum / mean_count
         lam = 0.5 if (m <= 0 or inc_f <= 0) else min(1.0, max(1e-6, inc_f / m))
     traj = [(0, inc_f)]
+    pool = []
     for rnd in range(1, rounds + 1):
         t0 = (rnd - 1) * K
         best_key, best = -1, None
-        Xs = shards(lambda r: diversify(inc_x, t0, len(range(r, K, world)), r, world))
+        if div == "blend" and pool:
+            P = np.stack(pool)
+            Xs = shards(lambda r: blend(inc_x, P, t0, len(range(r, K, world)), r, world))
+        else:
+            Xs = shards(lambda r: diversify(inc_x, t0, len(range(r, K, world)), r, world))
         fs = [eval_batch(Q, Xr, nthreads) for Xr in Xs]
         batch_max = max(int(fr.max()) for fr in fs if fr.size)
         T = threshold(lam, mean_sum, mean_count, max(inc_f, batch_max))
@@ -224,9 +259,14 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
                 key = max_key(int(fa[i]), r + int(slot) * world)
                 if key > best_key:
                     best_key, best = key, (int(fa[i]), Xa[i].copy())
+        improved_from = None
         if best is not None and best[0] > inc_f:
+            improved_from = inc_x
             inc_f, inc_x = best
             traj.append((rnd, inc_f))
+        if div == "blend":
+            pool = pool_update(pool, pool_cap, inc_x, improved_from,
+                               None if best is None else best[1])
     return inc_f, inc_x, traj
 
 

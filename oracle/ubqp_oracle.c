@@ -167,6 +167,31 @@ void oracle_diversify(int n, const uint8_t *seed, int64_t t0, int64_t k_local, i
 }
 
 /* ------------------------------------------------------------------------- */
+/* O4b blend ("diversification approaches based on blending (or breeding) two  */
+/*     solutions"; reading R11b).  Parent p = parents[g mod P]; */
+/*     (h, q, c) from t = t0 + g as in O4; the child takes p's bit on the mask  */
+/*     M(h,q) = {q-1, q-1+h, ...} (its complement within n bits when c = 1) and */
+/*     the seed's (incumbent's) bit everywhere else.  With p = NOT seed this is */
+/*     exactly O4.                                                               */
+/* ------------------------------------------------------------------------- */
+void oracle_blend(int n, const uint8_t *seed, const uint8_t *parents, int64_t n_parents, int64_t t0,
+                  int64_t k_local, int rank, int world, uint8_t *X)
+{
+    for (int64_t i = 0; i < k_local; ++i) {
+        int64_t g = (int64_t)rank + i * (int64_t)world;
+        const uint8_t *p = parents + (g % n_parents) * (int64_t)n;
+        int64_t h, q; int c;
+        oracle_glover_params(t0 + g, n, &h, &q, &c);
+        uint8_t *x = X + i * n;
+        for (int j = 0; j < n; ++j) {
+            int in_m = (j >= q - 1) && ((j - (q - 1)) % h == 0);
+            int take_parent = c == 1 ? !in_m : in_m;
+            x[j] = take_parent ? p[j] : seed[j];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
 /* O5  batch statistics {sum f, count, max_key}  (R14)            */
 /*     max_key = ((f + 2^40) << 22) | (2^22 - 1 - g): highest f, then lowest g */
 /* ------------------------------------------------------------------------- */

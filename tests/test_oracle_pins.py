@@ -193,6 +193,77 @@ def test_glover_sharding_is_cyclic():
                                   full[r::world])
 
 
+# ---------------------------------------------------------------- O4b blend (R11b)
+def test_blend_hand_worked_example():
+    n = 10
+    seed = np.zeros(n, np.uint8)
+    parent = np.array([1, 1, 1, 1, 1, 0, 0, 0, 0, 0], np.uint8)
+    for line in (GOLD / "blend_n10.txt").read_text().splitlines():
+        if line.startswith("#") or not line.strip():
+            continue
+        t, h, q, c, bits = line.split()
+        assert oracle.glover_params(int(t), n) == (int(h), int(q), int(c))
+        x = oracle.blend(seed, parent[None, :], int(t), 1)[0]
+        assert "".join(map(str, x.tolist())) == bits, line
+
+
+def test_blend_with_complement_parent_is_glover():
+    # parent = NOT seed: the child flips exactly the mask, i.e. O4 (pinned to Glover's
+    # printed illustration above) -- a wrong mask, shift or complement rule fails here
+    rng = np.random.default_rng(21)
+    for n in (10, 37, 130):
+        seed = rng.integers(0, 2, size=n).astype(np.uint8)
+        for t0 in (0, 7, n * (n + 1) - 3):
+            a = oracle.blend(seed, (1 - seed)[None, :], t0, 150)
+            b = oracle.diversify(seed, t0, 150)
+            assert np.array_equal(a, b), (n, t0)
+
+
+def test_blend_identity_and_shortest_path_property():
+    rng = np.random.default_rng(22)
+    n = 83
+    seed = rng.integers(0, 2, size=n).astype(np.uint8)
+    assert np.array_equal(oracle.blend(seed, seed[None, :], 0, 40), np.tile(seed, (40, 1)))
+    parents = rng.integers(0, 2, size=(3, n)).astype(np.uint8)
+    K = 400
+    X = oracle.blend(seed, parents, 11, K)
+    for g in range(K):
+        p = parents[g % 3]
+        x = X[g]
+        # the child lies on a shortest seed-parent path and keeps every agreed bit
+        assert int((x != seed).sum()) + int((x != p).sum()) == int((seed != p).sum())
+        assert np.array_equal(x[seed == p], seed[seed == p])
+        h, q, c = oracle.glover_params(11 + g, n)
+        inm = np.zeros(n, bool)
+        inm[q - 1::h] = True
+        take = ~inm if c else inm
+        assert int((x != seed).sum()) == int((take & (seed != p)).sum())
+
+
+def test_blend_sharding_is_cyclic():
+    n, K = 50, 29
+    rng = np.random.default_rng(23)
+    seed = rng.integers(0, 2, size=n).astype(np.uint8)
+    parents = rng.integers(0, 2, size=(4, n)).astype(np.uint8)
+    full = oracle.blend(seed, parents, 5, K)
+    for world in (2, 3):
+        for r in range(world):
+            assert np.array_equal(oracle.blend(seed, parents, 5, len(range(r, K, world)), r, world),
+                                  full[r::world])
+
+
+def test_pool_update_rules():
+    a, b, c, inc = (np.array(v, np.uint8) for v in ([1, 0], [0, 1], [1, 1], [0, 0]))
+    pool = oracle.pool_update([], 2, inc, None, a)           # round best joins
+    assert len(pool) == 1 and np.array_equal(pool[0], a)
+    assert len(oracle.pool_update(pool, 2, inc, None, inc)) == 1   # equal to the incumbent
+    assert len(oracle.pool_update(pool, 2, inc, None, a)) == 1     # already pooled
+    pool = oracle.pool_update(pool, 2, c, b, c)              # improved: the old incumbent b joins
+    assert [p.tolist() for p in pool] == [[1, 0], [0, 1]]
+    pool = oracle.pool_update(pool, 2, inc, None, c)         # capacity: oldest leaves
+    assert [p.tolist() for p in pool] == [[0, 1], [1, 1]]
+
+
 # ---------------------------------------------------------------- O5 stats
 def test_stats_sum_count_and_key_order():
     rng = np.random.default_rng(15)
@@ -327,6 +398,16 @@ def test_rounds_independent_of_world_size(world):
     a = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3, world=1)
     b = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3, world=world)
     assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2]
+
+
+def test_blend_rounds_improve_and_are_world_invariant():
+    Q = generate_Q(60, 0.5, -100, 100, seed=98)
+    a = oracle.run_rounds(Q, K=50, rounds=4, lam=0.4, max_flips=600, sample_seed=3, div="blend")
+    b = oracle.run_rounds(Q, K=50, rounds=4, lam=0.4, max_flips=600, sample_seed=3, world=3, div="blend")
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    assert a[0] == oracle.xQx(Q, a[1])
+    vals = [v for _, v in a[2]]
+    assert all(y > x for x, y in zip(vals, vals[1:]))
 
 
 # ---------------------------------------------------------------- input generator + layout
