@@ -99,6 +99,20 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max);
 int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_local,
                    int32_t rank, int32_t world);
 
+/* Blend diversification ("Different diversification approaches based on blending
+ * (or breeding) two solutions to generate new ones were implemented"; the operator is not
+ * printed -- DESIGN.md reading R11b).  Slot i (g = rank + i*world, t = t0 + g, (h, q, c)
+ * as in ubqp_diversify) takes parent p = parents[g mod n_parents]'s bits on the Glover
+ * mask M(h,q) (on its complement within n bits when c = 1) and seed_bits' elsewhere:
+ *   x = seed xor (mask_c and (p xor seed)).
+ * p = NOT seed reproduces ubqp_diversify exactly; p = seed gives the seed.  Every child
+ * lies on a shortest seed-p path (path relinking).  parents: n_parents * W64 words,
+ * host or device (host parents are staged in a handle-owned buffer, grown on demand,
+ * synchronising the stream when it grows); 1 <= n_parents <= 2^22.  Bits >= n of seed
+ * and parents are ignored.  Errors: E_INVALID, E_STATE (no Q), E_NOMEM. */
+int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int64_t n_parents,
+               int64_t t0, int64_t k_local, int32_t rank, int32_t world);
+
 /* EvaluateRandomStarts' random solutions: bit j of slot i is bit
  * (j & 63) of SplitMix64-mix(seed + (g*W64 + (j>>6) + 1) * 0x9E3779B97F4A7C15),
  * g = rank + i*world.  Fills the batch with k_local solutions. */

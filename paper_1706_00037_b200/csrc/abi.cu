@@ -80,7 +80,8 @@ void free_batch(Ctx &c) {
 
 void free_all(Ctx &c) {
     free_batch(c);
-    dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.scratch64);
+    dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents);
+    c.parents_cap = 0; dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
     dfree(c.fs); dfree(c.fint); dfree(c.freal);
     c.real = false;
@@ -325,6 +326,44 @@ int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_lo
     h->k_local = k_local;
     h->f_valid = h->gains_valid = false;
     ubqp::launch_glover(*h, seed_dev, t0, k_local);
+    CK_LAUNCH("glover_kernel");
+    return UBQP_OK;
+}
+
+int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int64_t n_parents, int64_t t0,
+               int64_t k_local, int32_t rank, int32_t world) {
+    GUARD(h);
+    int rc = check_batch_args(h, k_local, rank, world);
+    if (rc) return rc;
+    if (!seed_bits || !parents) return fail(h, UBQP_E_INVALID, "ubqp: seed_bits or parents is NULL");
+    if (n_parents < 1 || n_parents > (1ll << 22)) return fail(h, UBQP_E_INVALID, "ubqp: n_parents must be in [1, 2^22]");
+    if (t0 < 0) return fail(h, UBQP_E_INVALID, "ubqp: t0 < 0");
+    const uint64_t *seed_dev = seed_bits;
+    if (!is_device_ptr(seed_bits)) {
+        CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+        seed_dev = h->seed;
+    }
+    const uint64_t *par_dev = parents;
+    if (!is_device_ptr(parents)) {
+        if (n_parents > h->parents_cap) {
+            CK(cudaStreamSynchronize(h->stream));
+            dfree(h->parents);
+            h->parents_cap = 0;
+            if (cudaMalloc(&h->parents, n_parents * h->W64 * sizeof(uint64_t)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the parents buffer");
+            }
+            h->parents_cap = n_parents;
+        }
+        CK(cudaMemcpyAsync(h->parents, parents, n_parents * h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                           h->stream));
+        par_dev = h->parents;
+    }
+    h->rank = rank;
+    h->world = world;
+    h->k_local = k_local;
+    h->f_valid = h->gains_valid = false;
+    ubqp::launch_glover(*h, seed_dev, t0, k_local, par_dev, n_parents);
     CK_LAUNCH("glover_kernel");
     return UBQP_OK;
 }

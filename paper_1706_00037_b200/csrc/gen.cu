@@ -42,7 +42,13 @@ __device__ __forceinline__ int64_t isqrt_dev(int64_t v) {
     return s;
 }
 
-__global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict__ seed, int64_t t0,
+// parents == nullptr: Glover (O4), x = seed xor M(h,q), complemented within n iff c = 1.
+// parents != nullptr: blend (O4b, R11b), x takes parent[g mod P]'s bits on the mask (its
+// complement when c = 1) and the seed's elsewhere: x = seed xor (mask_c & (p xor seed)).
+// p = NOT seed gives back the Glover word: seed xor mask_c = seed xor M, complemented iff c.
+__global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict__ seed,
+                                                     const uint64_t *__restrict__ parents,
+                                                     int64_t n_parents, int64_t t0,
                                                      int64_t k, int rank, int world, int n,
                                                      int W64, int NW, int n_pad,
                                                      uint64_t *__restrict__ Xb,
@@ -68,9 +74,9 @@ __global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict_
         uint64_t mask = 0;
         const int64_t hi = lo + 64 < n ? lo + 64 : n;
         for (; j < hi; j += h) mask |= 1ull << (j - lo);
-        word = seed[w] ^ mask;
-        if (comp) word = ~word;
-        word &= tail_mask(n, w);
+        const uint64_t sw = seed[w];
+        const uint64_t diff = parents ? parents[(g % n_parents) * W64 + w] ^ sw : ~0ull;
+        word = (sw ^ ((comp ? ~mask : mask) & diff)) & tail_mask(n, w);
         Xb[slot * W64 + w] = word;
     }
     store_expanded(X8 + slot * n_pad + 64ll * w, word);
@@ -148,10 +154,12 @@ inline unsigned blocks_for(int64_t threads) { return static_cast<unsigned>((thre
 
 }  // namespace
 
-void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k) {
+void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k, const uint64_t *parents_dev,
+                   int64_t n_parents) {
     if (k <= 0) return;
     const int NW = c.n_pad / 64;
-    glover_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed_dev, t0, k, c.rank, c.world, c.n,
+    glover_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed_dev, parents_dev, n_parents, t0, k, c.rank,
+                                                            c.world, c.n,
                                                             c.W64, NW, c.n_pad, c.Xb, c.X8);
     ++c.launches;
 }

@@ -36,6 +36,8 @@ struct Ctx {
     int8_t *Q8 = nullptr;        // [q_rows][q_ld] row-major, zero padded; row k = column k (Q = Q^t)
     int32_t *diag = nullptr;     // [q_rows]
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
+    uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
+    int64_t parents_cap = 0;
     // batch workspace
     int64_t k_max = 0, k_cap_pad = 0, k_local = -1;
     int rank = 0, world = 1;
@@ -74,7 +76,9 @@ struct Ctx {
 
 // ------------------------------------------------------------------ launchers (host)
 // gen.cu
-void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k);
+// parents_dev == nullptr: Glover (O4); else blend with parents_dev[(g mod n_parents)] (O4b)
+void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k,
+                   const uint64_t *parents_dev = nullptr, int64_t n_parents = 0);
 void launch_random(Ctx &c, uint64_t seed, int64_t k);
 void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
 void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer or real planes

@@ -80,6 +80,18 @@ def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None):
     return k, out
 
 
+def pool_update(pool: list, pool_cap: int, inc_bits: torch.Tensor, improved_from, round_best) -> list:
+    """Parent pool of the blend policy (R11b): distinct local optima other than
+    the incumbent, oldest first, at most pool_cap.  After a round the replaced incumbent
+    (improved_from), else the round's best ascended solution, joins unless it equals the
+    incumbent or is already pooled.  Every rank holds the same pool (the round best is
+    broadcast by combine_best), so the blend stays independent of the world size (O10)."""
+    cand = improved_from if improved_from is not None else round_best
+    if cand is None or torch.equal(cand, inc_bits) or any(torch.equal(cand, p) for p in pool):
+        return pool
+    return (pool + [cand.clone()])[-pool_cap:]
+
+
 @dataclass
 class RoundResult:
     m: int            # survivors on this rank
@@ -138,10 +150,15 @@ class MultiStart:
         s = self.stats.tolist()
         return s[0], s[1]
 
-    def round(self, seed_bits: torch.Tensor, t0: int, inc_f: int, mean=None) -> RoundResult:
-        """One batched round.  mean=None -> the batch's own mean (R5)."""
+    def round(self, seed_bits: torch.Tensor, t0: int, inc_f: int, mean=None,
+              parents: torch.Tensor | None = None) -> RoundResult:
+        """One batched round.  mean=None -> the batch's own mean (R5).
+        parents [P][W64] (device): blend diversification (O4b) instead of Glover (O4)."""
         u = self.u
-        u.diversify(seed_bits, t0, self.k_local, self.rank, self.world)
+        if parents is None:
+            u.diversify(seed_bits, t0, self.k_local, self.rank, self.world)
+        else:
+            u.blend(seed_bits, parents, int(parents.shape[0]), t0, self.k_local, self.rank, self.world)
         u.eval_batch(UBQP_EMIT_GAINS, None, self.stats)
         combine_stats(self.stats, self.group)
         ssum, scount, skey, _ = self.stats.tolist()
@@ -167,20 +184,30 @@ class MultiStart:
             best_bits = self.bits[i].clone()
         return RoundResult(m, T, best_key, best_bits, batch_max, mean_sum, mean_count)
 
-    def run(self, rounds: int, sample_seed: int, t_start: int = 0, lam_policy: str = "fixed"):
+    def run(self, rounds: int, sample_seed: int, t_start: int = 0, lam_policy: str = "fixed",
+            div: str = "glover", pool_cap: int = 8):
         """Figure 2 as batched rounds (O8): pinned sampling mean, first-derivative
         incumbent, rounds of diversify/eval/screen/ascend; strict improvement.
         lam_policy "paper": lambda = Max/Mean = Starting_solution/Mean, clamped to
-        (0, 1] with 0.5 when Mean <= 0 or the start's value <= 0 (R7)."""
+        (0, 1] with 0.5 when Mean <= 0 or the start's value <= 0 (R7).
+        div "blend": once the parent pool is non-empty, rounds blend the incumbent with
+        pool[g mod P] (O4b) instead of Glover's generator."""
         mean = self.sample_mean(sample_seed)
         inc_bits, inc_f = self.first_derivative()
         if lam_policy == "paper":
             self.lam = paper_lambda(mean[0] / mean[1], inc_f)
         traj = [(0, inc_f)]
+        pool: list = []
         for r in range(1, rounds + 1):
-            res = self.round(inc_bits, t_start + (r - 1) * self.K, inc_f, mean)
+            parents = torch.stack(pool) if (div == "blend" and pool) else None
+            res = self.round(inc_bits, t_start + (r - 1) * self.K, inc_f, mean, parents=parents)
+            improved_from = None
             if res.best_key >= 0 and key_f(res.best_key) > inc_f:
+                improved_from = inc_bits
                 inc_f = key_f(res.best_key)
                 inc_bits = res.best_bits.clone()
                 traj.append((r, inc_f))
+            if div == "blend":
+                pool = pool_update(pool, pool_cap, inc_bits, improved_from,
+                                   res.best_bits if res.best_key >= 0 else None)
         return inc_f, inc_bits, traj

@@ -22,7 +22,7 @@ Q_N, Q_NPAD, Q_W64, Q_KMAX, Q_KLOCAL, Q_LAUNCHES, Q_STREAM = range(7)
 
 # every entry point declared in include/ubqp.h
 EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ubqp_load_Q",
-           "ubqp_diversify", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
+           "ubqp_diversify", "ubqp_blend", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
            "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_sync", "ubqp_query",
            "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real"]
 UBQP_F32, UBQP_F64 = 1, 2
@@ -67,6 +67,7 @@ def load_library(path: Path | str | None = None):
         "ubqp_last_error": ([P], ctypes.c_char_p),
         "ubqp_load_Q": ([P, i32, P, i64], ctypes.c_int),
         "ubqp_diversify": ([P, P, i64, i64, i32, i32], ctypes.c_int),
+        "ubqp_blend": ([P, P, P, i64, i64, i64, i32, i32], ctypes.c_int),
         "ubqp_random": ([P, u64, i64, i32, i32], ctypes.c_int),
         "ubqp_set_batch": ([P, P, i64, i32, i32], ctypes.c_int),
         "ubqp_get_batch": ([P, P], ctypes.c_int),
@@ -155,6 +156,9 @@ class Ubqp:
 
     def diversify(self, seed_bits, t0: int, k_local: int, rank: int = 0, world: int = 1):
         self._ck(self.lib.ubqp_diversify(self.h, _ptr(seed_bits), t0, k_local, rank, world))
+
+    def blend(self, seed_bits, parents, n_parents: int, t0: int, k_local: int, rank: int = 0, world: int = 1):
+        self._ck(self.lib.ubqp_blend(self.h, _ptr(seed_bits), _ptr(parents), n_parents, t0, k_local, rank, world))
 
     def random(self, seed: int, k_local: int, rank: int = 0, world: int = 1):
         self._ck(self.lib.ubqp_random(self.h, seed & (2**64 - 1), k_local, rank, world))

@@ -64,6 +64,43 @@ def test_glover_batch_bits(n):
 
 
 @pytest.mark.parametrize("n", NS)
+def test_blend_batch_bits(n):
+    """O4b blend (R11b) bit-exact, host and device parents, P in {1, 3, > K}, sharded."""
+    Q = generate_Q(n, 0.5, seed=n)
+    K = 333
+    rng = np.random.default_rng(100 + n)
+    seed_x = rng.integers(0, 2, size=n).astype(np.uint8)
+    u = _handle_with(Q, K)
+    for P in (1, 3, 400):
+        parents = rng.integers(0, 2, size=(P, n)).astype(np.uint8)
+        pb = pack_bits(parents)
+        for t0 in (0, 3 * n * (n + 1) + 11):
+            u.blend(pack_bits(seed_x)[0], pb, P, t0, K)
+            assert np.array_equal(_batch(u, K, n), oracle.blend(seed_x, parents, t0, K)), (P, t0)
+        pd = torch.from_numpy(pb.view(np.int64)).cuda()
+        for world in (1, 3):
+            for r in range(world):
+                kl = len(range(r, K, world))
+                u.blend(pack_bits(seed_x)[0], pd, P, 9, kl, r, world)
+                torch.cuda.synchronize()
+                assert np.array_equal(_batch(u, kl, n), oracle.blend(seed_x, parents, 9, kl, r, world)), (P, r)
+
+
+def test_blend_complement_parent_equals_glover_and_errors():
+    n, K = 777, 500
+    Q = generate_Q(n, 0.5, seed=3)
+    rng = np.random.default_rng(5)
+    seed_x = rng.integers(0, 2, size=n).astype(np.uint8)
+    u = _handle_with(Q, K)
+    u.blend(pack_bits(seed_x)[0], pack_bits((1 - seed_x)[None, :]), 1, 40, K)
+    a = _batch(u, K, n)
+    u.diversify(pack_bits(seed_x)[0], 40, K)
+    assert np.array_equal(a, _batch(u, K, n))
+    with pytest.raises(UbqpError):
+        u.blend(pack_bits(seed_x)[0], pack_bits(seed_x[None, :]), 0, 0, K)
+
+
+@pytest.mark.parametrize("n", NS)
 @pytest.mark.parametrize("density", [0.1, 1.0])
 def test_eval_f_and_stats(n, density):
     Q = generate_Q(n, density, seed=7 * n + 1)
@@ -392,6 +429,18 @@ def test_multistart_paper_lambda_matches_oracle():
     best, bits, traj = ms.run(3, sample_seed=9, lam_policy="paper")
     obest, ox, otraj = oracle.run_rounds(Q, K, 3, "paper", 10 * n, sample_seed=9, nthreads=8)
     assert best == obest and traj == otraj
+
+
+@pytest.mark.parametrize("n,K,rounds,lam", [(60, 400, 5, 0.4), (300, 2000, 4, 0.3)])
+def test_multistart_blend_matches_oracle(n, K, rounds, lam):
+    """Figure-2 driver with blend diversification (NEXT-2, R11b) against the oracle."""
+    from paper_1706_00037_b200.multistart import MultiStart
+    Q = generate_Q(n, 0.5, seed=200 + n)
+    ms = MultiStart(Q, K, lam=lam, max_flips=10 * n)
+    best, bits, traj = ms.run(rounds, sample_seed=4, div="blend")
+    obest, ox, otraj = oracle.run_rounds(Q, K, rounds, lam, 10 * n, sample_seed=4, nthreads=8, div="blend")
+    assert best == obest and traj == otraj
+    assert np.array_equal(unpack_bits(bits.cpu().numpy().view(np.uint64), n)[0], ox)
 
 
 @pytest.mark.parametrize("n", [16384])

@@ -89,3 +89,23 @@ def test_key_helpers_match_oracle():
     for f, g in ((0, 0), (-5, 17), (10**9, (1 << 22) - 1), (-(1 << 39), 3)):
         k = oracle.max_key(f, g)
         assert key_f(k) == f and key_g(k) == g
+
+
+def test_blend_pool_update_matches_oracle_rules():
+    """Host logic of the blend policy: multistart.pool_update on packed torch bits makes the
+    same decisions as the oracle's pool_update on unpacked arrays (R11b)."""
+    from paper_1706_00037_b200.multistart import pool_update
+    rng = np.random.default_rng(31)
+    n = 70
+    sols = [rng.integers(0, 2, size=n).astype(np.uint8) for _ in range(5)]
+    pool_o, pool_t = [], []
+    for step in range(60):
+        inc = sols[rng.integers(0, 5)]
+        imp = sols[rng.integers(0, 5)] if rng.random() < 0.4 else None
+        rb = sols[rng.integers(0, 5)] if rng.random() < 0.8 else None
+        pool_o = oracle.pool_update(pool_o, 3, inc, imp, rb)
+        tb = (lambda x: None if x is None else torch.from_numpy(pack_bits(x)[0].view(np.int64)))
+        pool_t = pool_update(pool_t, 3, tb(inc), tb(imp), tb(rb))
+        assert len(pool_o) == len(pool_t)
+        for a, b in zip(pool_o, pool_t):
+            assert np.array_equal(pack_bits(a)[0].view(np.int64), b.numpy())
