@@ -21,7 +21,7 @@ _lib = None
 __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
-    "first_derivative_start", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
+    "first_derivative_start", "relink", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
 ]
 
 
@@ -61,6 +61,7 @@ def _L():
         lib.oracle_screen.restype = i64
         lib.oracle_ascend_batch.argtypes = [i32, P, i64, P, P, P, i32, i32]
         lib.oracle_first_derivative_start.argtypes = [i32, P, P]
+        lib.oracle_relink_batch.argtypes = [i32, P, i64, P, P, P, i64, P, P, P, P, P, i32]
         _lib = lib
     return _lib
 
@@ -198,6 +199,29 @@ def ascend(Q, X, f, max_flips: int, nthreads: int = 1):
     _L().oracle_ascend_batch(n, _p(Q), X.shape[0], _p(X), _p(f), _p(flips), int(max_flips),
                              int(nthreads))
     return X, f, flips
+
+
+# O11 -- path relinking from X0 toward guides (R19)
+def relink(Q, X0, f0, guides, nthreads: int = 1, with_path: bool = False):
+    """Returns (Xbest uint8 [m][n], fbest int64 [m] (INT64_MIN: none), sbest int32 [m]
+    (-1: none), length |D| int32 [m][, path int32 [m][n] flip order]); guide of row i is
+    guides[i mod len(guides)]."""
+    Q = _Q(Q)
+    n = Q.shape[0]
+    X0 = _X(X0, n)
+    Y = _X(guides, n)
+    m = X0.shape[0]
+    f0 = np.ascontiguousarray(f0, dtype=np.int64)
+    Xb = np.zeros_like(X0)
+    fb = np.zeros(m, np.int64)
+    sb = np.zeros(m, np.int32)
+    ln = np.zeros(m, np.int32)
+    path = np.full((m, n), -1, np.int32) if with_path else None
+    rc = _L().oracle_relink_batch(n, _p(Q), m, _p(X0), _p(f0), _p(Y), Y.shape[0], _p(Xb), _p(fb), _p(sb),
+                                  _p(ln), _p(path) if with_path else None, int(nthreads))
+    if rc:
+        raise ValueError("oracle_relink_batch: bad arguments")
+    return (Xb, fb, sb, ln, path) if with_path else (Xb, fb, sb, ln)
 
 
 # first-derivative start (P:55, P:68, P:91; S:232-240)

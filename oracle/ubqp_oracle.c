@@ -21,6 +21,8 @@
  *   O4 (Glover diversification): pinned only by Glover's own x = 0 example and
  *   the definition; the paper prints no vectors ("parity unpinned by the paper").
  *   O8 (round loop) quality vs Tables 1'/2: parity unpinned (no instance files).
+ *   O4b (blend) and O11 (path relinking) are readings R11b / R19 of passages that
+ *   print no operator; pinned by reductions, invariants, brute force and hand tables.
  */
 #include <math.h>
 #include <pthread.h>
@@ -294,6 +296,97 @@ int oracle_ascend_batch(int n, const int32_t *Q, int64_t m, uint8_t *X, int64_t 
         if (jobs[t].begin >= jobs[t].end) break;
         if (nthreads == 1) { ascend_worker(&jobs[t]); continue; }
         pthread_create(&th[t], NULL, ascend_worker, &jobs[t]);
+        ++started;
+    }
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O11 path relinking (NEXT-4: Glover's "Scatter Search / Path Relinking      */
+/*     Phase"; the paper defers "solution polishing";      */
+/*     DESIGN.md reading R19).  From x0 toward the guide y: D = {j: x0_j !=   */
+/*     y_j}; |D| forced steps, each flipping the j in D of largest gain       */
+/*     Delta_j (lowest j on ties; the move may worsen f), D -= {j}, gains     */
+/*     updated as in O7.  Result: the best strictly interior point (1 <= s <  */
+/*     |D|; highest f, earliest s on ties); s_best = -1 when |D| < 2.         */
+/* ------------------------------------------------------------------------- */
+static void relink_one(int n, const int32_t *Q, const uint8_t *x0, const uint8_t *y, int64_t f0,
+                       uint8_t *xbest, int64_t *fbest, int32_t *sbest, int32_t *len, int32_t *path,
+                       int64_t *Delta, uint8_t *x, uint8_t *D)
+{
+    int nd = 0;
+    for (int j = 0; j < n; ++j) {
+        x[j] = x0[j];
+        xbest[j] = x0[j];
+        D[j] = (uint8_t)(x0[j] != y[j]);
+        nd += D[j];
+    }
+    oracle_gains(n, Q, x, Delta);
+    int64_t f = f0;
+    *fbest = INT64_MIN;
+    *sbest = -1;
+    *len = nd;
+    for (int s = 1; s <= nd; ++s) {
+        int k = -1;
+        for (int j = 0; j < n; ++j)
+            if (D[j] && (k < 0 || Delta[j] > Delta[k])) k = j;   /* strict: lowest j on ties */
+        f += Delta[k];
+        int64_t d = 1 - 2 * (int64_t)x[k];
+        x[k] = (uint8_t)(1 - x[k]);
+        D[k] = 0;
+        for (int l = 0; l < n; ++l)
+            if (l != k)
+                Delta[l] += 2 * (int64_t)Q[(int64_t)l * n + k] * d * (1 - 2 * (int64_t)x[l]);
+        Delta[k] = -Delta[k];
+        if (path) path[s - 1] = k;
+        if (s < nd && f > *fbest) {
+            *fbest = f;
+            *sbest = s;
+            for (int j = 0; j < n; ++j) xbest[j] = x[j];
+        }
+    }
+}
+
+typedef struct {
+    int n; const int32_t *Q; const uint8_t *X0; const int64_t *f0; const uint8_t *Y; int64_t n_guides;
+    uint8_t *Xb; int64_t *fb; int32_t *sb; int32_t *len; int32_t *path; int64_t begin, end;
+} relink_job;
+
+static void *relink_worker(void *arg)
+{
+    relink_job *j = (relink_job *)arg;
+    size_t nn = (size_t)(j->n > 0 ? j->n : 1);
+    int64_t *Delta = (int64_t *)malloc(sizeof(int64_t) * nn);
+    uint8_t *x = (uint8_t *)malloc(nn), *D = (uint8_t *)malloc(nn);
+    for (int64_t i = j->begin; i < j->end; ++i)
+        relink_one(j->n, j->Q, j->X0 + i * (int64_t)j->n, j->Y + (i % j->n_guides) * (int64_t)j->n, j->f0[i],
+                   j->Xb + i * (int64_t)j->n, &j->fb[i], &j->sb[i], &j->len[i],
+                   j->path ? j->path + i * (int64_t)j->n : NULL, Delta, x, D);
+    free(Delta); free(x); free(D);
+    return NULL;
+}
+
+/* X0[m][n] initiating solutions with values f0[m]; guide of i = Y[i mod n_guides];
+ * out: Xb[m][n] best interior points, fb[m] (INT64_MIN if none), sb[m] (-1 if none),
+ * len[m] = |D|, path[m][n] flip order (optional, may be NULL). */
+int oracle_relink_batch(int n, const int32_t *Q, int64_t m, const uint8_t *X0, const int64_t *f0,
+                        const uint8_t *Y, int64_t n_guides, uint8_t *Xb, int64_t *fb, int32_t *sb,
+                        int32_t *len, int32_t *path, int nthreads)
+{
+    if (n < 1 || m < 0 || n_guides < 1) return 1;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    relink_job jobs[256];
+    int64_t per = (m + nthreads - 1) / nthreads;
+    int started = 0;
+    for (int t = 0; t < nthreads; ++t) {
+        jobs[t] = (relink_job){n, Q, X0, f0, Y, n_guides, Xb, fb, sb, len, path, (int64_t)t * per, 0};
+        jobs[t].end = jobs[t].begin + per > m ? m : jobs[t].begin + per;
+        if (jobs[t].begin >= jobs[t].end) break;
+        if (nthreads == 1) { relink_worker(&jobs[t]); continue; }
+        pthread_create(&th[t], NULL, relink_worker, &jobs[t]);
         ++started;
     }
     for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);

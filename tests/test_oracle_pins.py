@@ -264,6 +264,74 @@ def test_pool_update_rules():
     assert [p.tolist() for p in pool] == [[0, 1], [1, 1]]
 
 
+# ---------------------------------------------------------------- O11 path relinking (R19)
+def test_relink_hand_worked_q3():
+    Q = _Qn("Q3")
+    for line in (GOLD / "relink_q3.txt").read_text().splitlines():
+        if line.startswith("#") or not line.strip():
+            continue
+        x0, y, path, fb, sb, xb = line.split()
+        x0 = np.array([int(c) for c in x0], np.uint8)
+        y = np.array([int(c) for c in y], np.uint8)
+        Xb, f, s, ln, P = oracle.relink(Q, x0, [oracle.xQx(Q, x0)], y, with_path=True)
+        assert P[0][:ln[0]].tolist() == [int(v) for v in path.split(",")], line
+        assert (int(f[0]), int(s[0]), "".join(map(str, Xb[0].tolist()))) == (int(fb), int(sb), xb), line
+
+
+def _brute_walk(Q, x0, y):
+    """the walk by brute-force objective evaluation of every candidate move (O1 only)"""
+    x = x0.copy()
+    D = [j for j in range(len(x)) if x0[j] != y[j]]
+    fs, path = [], []
+    while D:
+        best = None
+        for j in D:                                   # ascending j: strict > keeps the lowest
+            x[j] ^= 1
+            v = oracle.xQx(Q, x)
+            x[j] ^= 1
+            if best is None or v > best[0]:
+                best = (v, j)
+        x[best[1]] ^= 1
+        D.remove(best[1])
+        fs.append(best[0])
+        path.append(best[1])
+    return fs, path
+
+
+def test_relink_equals_brute_force_walk():
+    rng = np.random.default_rng(41)
+    for trial in range(30):
+        n = int(rng.integers(2, 14))
+        Q = generate_Q(n, 0.6, -20, 20, seed=1000 + trial)
+        X0 = rng.integers(0, 2, size=(4, n)).astype(np.uint8)
+        Y = rng.integers(0, 2, size=(3, n)).astype(np.uint8)
+        f0 = oracle.eval_batch(Q, X0)
+        Xb, fb, sb, ln, P = oracle.relink(Q, X0, f0, Y, with_path=True)
+        for i in range(4):
+            y = Y[i % 3]
+            fs, path = _brute_walk(Q, X0[i], y)
+            assert ln[i] == len(path) and P[i][:ln[i]].tolist() == path
+            if len(path) < 2:
+                assert sb[i] == -1 and np.array_equal(Xb[i], X0[i])
+                continue
+            inner = fs[:-1]
+            s = int(np.argmax(inner))                 # first maximum = earliest step
+            assert (int(fb[i]), int(sb[i])) == (inner[s], s + 1)
+            assert oracle.xQx(Q, Xb[i]) == fb[i]
+            assert int((Xb[i] != X0[i]).sum()) == sb[i] and int((Xb[i] != y).sum()) == ln[i] - sb[i]
+            if fs:
+                assert fs[-1] == oracle.xQx(Q, y)     # the walk ends at the guide
+
+
+def test_relink_zero_Q_flips_in_index_order():
+    n = 9
+    Q = np.zeros((n, n), np.int32)
+    x0 = np.zeros(n, np.uint8)
+    y = np.array([1, 0, 1, 1, 0, 0, 1, 0, 1], np.uint8)
+    Xb, fb, sb, ln, P = oracle.relink(Q, x0, [0], y, with_path=True)
+    assert P[0][:5].tolist() == [0, 2, 3, 6, 8] and (fb[0], sb[0]) == (0, 1)
+
+
 # ---------------------------------------------------------------- O5 stats
 def test_stats_sum_count_and_key_order():
     rng = np.random.default_rng(15)
