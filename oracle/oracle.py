@@ -21,7 +21,7 @@ _lib = None
 __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
-    "first_derivative_start", "relink", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
+    "first_derivative_start", "relink", "polish", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
 ]
 
 
@@ -232,9 +232,33 @@ def first_derivative_start(Q) -> np.ndarray:
     return x
 
 
+# polish phase over an elite set (NEXT-4; R19): relink every ordered pair, ascend the interior
+def polish(Q, elite, max_flips: int, nthreads: int = 1):
+    """elite uint8 [E][n].  Every ordered pair (a, b), a != b, in row-major order is relinked
+    from elite[a] toward elite[b] (O11); the best interior points (pairs with one) are
+    ascended (O7) in pair order; returns (f, x) of the best result (highest f, then the
+    earliest pair) or None when no pair has an interior point."""
+    Q = _Q(Q)
+    n = Q.shape[0]
+    E = _X(elite, n)
+    pairs = [(a, b) for a in range(E.shape[0]) for b in range(E.shape[0]) if a != b]
+    if not pairs:
+        return None
+    X0 = np.stack([E[a] for a, _ in pairs])
+    Y = np.stack([E[b] for _, b in pairs])
+    Xb, fb, sb, _ = relink(Q, X0, eval_batch(Q, X0, nthreads), Y, nthreads)
+    idx = np.flatnonzero(sb >= 0)
+    if idx.size == 0:
+        return None
+    Xa, fa, _ = ascend(Q, Xb[idx], fb[idx], max_flips, nthreads)
+    best = max(range(idx.size), key=lambda i: max_key(int(fa[i]), i))
+    return int(fa[best]), Xa[best].copy()
+
+
 # O8 -- batched rounds of Figure 2 (P:63-87; R5, R6, R13)
 def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
-               world: int = 1, nthreads: int = 1, div: str = "glover", pool_cap: int = 8):
+               world: int = 1, nthreads: int = 1, div: str = "glover", pool_cap: int = 8,
+               polish_end: bool = False):
     """Round 0: K random starts (O3, seed ``sample_seed``) -> pinned (mean_sum, mean_count)
     (P:55 "the mean is the average xQx value derived during sampling").  Incumbent =
     first-derivative start.  Round r >= 1: diversify from the incumbent with
@@ -243,7 +267,9 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
     best ascended f is strictly greater, ties -> lowest g (R8, R14).
     ``world`` shards every batch cyclically (O10); results must not depend on it.
     ``div`` "blend": once the parent pool (pool_update) is non-empty, rounds blend the
-    incumbent with pool[g mod P] (O4b) instead of O4.
+    incumbent with pool[g mod P] (O4b) instead of O4.  ``polish_end``: after the last
+    round, polish(pool + [incumbent]) (O11 + O7); a strictly better result is recorded as
+    round ``rounds + 1``.
     Returns (best_value, best_x, trajectory[list of (round, best_value)])."""
     Q = _Q(Q)
     n = Q.shape[0]
@@ -288,9 +314,14 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
             improved_from = inc_x
             inc_f, inc_x = best
             traj.append((rnd, inc_f))
-        if div == "blend":
+        if div == "blend" or polish_end:
             pool = pool_update(pool, pool_cap, inc_x, improved_from,
                                None if best is None else best[1])
+    if polish_end:
+        res = polish(Q, np.stack(pool + [inc_x]), max_flips, nthreads)
+        if res is not None and res[0] > inc_f:
+            inc_f, inc_x = res
+            traj.append((rounds + 1, inc_f))
     return inc_f, inc_x, traj
 
 

@@ -478,6 +478,40 @@ def test_blend_rounds_improve_and_are_world_invariant():
     assert all(y > x for x, y in zip(vals, vals[1:]))
 
 
+def test_polish_pairs_and_result_consistency():
+    rng = np.random.default_rng(51)
+    n = 40
+    Q = generate_Q(n, 0.5, -50, 50, seed=51)
+    E = rng.integers(0, 2, size=(4, n)).astype(np.uint8)
+    f, x = oracle.polish(Q, E, 10 * n)
+    assert f == oracle.xQx(Q, x)
+    g = oracle.gains(Q, x)
+    assert g.max() <= 0                               # an ascended point: 1-flip local optimum
+    # brute force over the pairs: the best of ascending each pair's best interior point
+    cands = []
+    for a in range(4):
+        for b in range(4):
+            if a == b:
+                continue
+            Xb, fb, sb, _ = oracle.relink(Q, E[a], [oracle.xQx(Q, E[a])], E[b])
+            if sb[0] >= 0:
+                Xa, fa, _ = oracle.ascend(Q, Xb, fb, 10 * n)
+                cands.append(int(fa[0]))
+    assert f == max(cands)
+    assert oracle.polish(Q, E[:1], 10 * n) is None    # no pairs
+    assert oracle.polish(Q, np.stack([E[0], E[0]]), 10 * n) is None   # |D| = 0
+
+
+def test_rounds_with_polish_keep_invariants():
+    Q = generate_Q(60, 0.5, -100, 100, seed=97)
+    a = oracle.run_rounds(Q, K=40, rounds=3, lam=0.4, max_flips=600, sample_seed=5, polish_end=True)
+    b = oracle.run_rounds(Q, K=40, rounds=3, lam=0.4, max_flips=600, sample_seed=5, world=2, polish_end=True)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1]) and a[2] == b[2]
+    assert a[0] == oracle.xQx(Q, a[1])
+    vals = [v for _, v in a[2]]
+    assert all(y > x for x, y in zip(vals, vals[1:]))
+
+
 # ---------------------------------------------------------------- input generator + layout
 def test_generator_symmetry_density_determinism():
     Q = generate_Q(100, 0.1, -100, 100, seed=1)
