@@ -170,6 +170,22 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
                 int64_t *f_out, int32_t *flips_out, uint64_t *bits_out,
                 int64_t *best_key_out);
 
+/* Path relinking (NEXT-4: Glover's scatter search / path relinking phase, which the
+ * paper defers as "solution polishing"; reading R19).  For i < m,
+ * from batch slot s = slots[i] (f and gains as for ubqp_ascend) toward the guide
+ * y = guides[i mod n_guides] (W64 words each, host or device): D = {j : x_j != y_j};
+ * |D| forced steps, each flipping the j in D of largest gain (lowest j on ties, even when
+ * the move worsens f), D -= {j}.  Outputs per i: f_out int64[m] = the best strictly
+ * interior value (1 <= step < |D|; highest f, earliest step on ties; INT64_MIN if |D| < 2),
+ * step_out int32[m] its step (-1 if none), len_out int32[m] = |D|, bits_out
+ * uint64[m][W64] that interior solution (the start itself if none), best_key_out = max
+ * over i with an interior point of max_key(f_i, g(s_i)) (-1 if none).  Any output may
+ * be NULL.  Requires (2n-1)*qmax < 2^21 (E_RANGE).  The batch is not modified.
+ * Errors: E_INVALID (slot out of range, m > k_local, n_guides < 1), E_STATE, E_RANGE. */
+int ubqp_relink(ubqp_t h, const uint64_t *guides, int64_t n_guides, const int32_t *slots,
+                int64_t m, int64_t *f_out, int32_t *step_out, int32_t *len_out,
+                uint64_t *bits_out, int64_t *best_key_out);
+
 /* ---------------------------------------------------------------------------------
  * Real-valued Q (a4': "Q ... of real or integer coefficients"; "float or double",
  * P:89).  The coefficients are rounded once to 28-bit fixed point,

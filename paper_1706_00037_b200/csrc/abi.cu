@@ -72,7 +72,7 @@ void dfree(T *&p) {
 
 void free_batch(Ctx &c) {
     dfree(c.Xb); dfree(c.X8); dfree(c.f); dfree(c.gains); dfree(c.surv); dfree(c.blk_count);
-    dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots);
+    dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots); dfree(c.asc_aux);
     c.asc_cap = 0;
     c.k_max = 0; c.k_cap_pad = 0; c.k_local = -1;
     c.f_valid = c.gains_valid = false;
@@ -80,8 +80,8 @@ void free_batch(Ctx &c) {
 
 void free_all(Ctx &c) {
     free_batch(c);
-    dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents);
-    c.parents_cap = 0; dfree(c.scratch64);
+    dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents); dfree(c.guides);
+    c.parents_cap = c.guides_cap = 0; dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
     dfree(c.fs); dfree(c.fint); dfree(c.freal);
     c.real = false;
@@ -133,10 +133,11 @@ int ensure_gains(ubqp_t h) {
 
 int ensure_asc(ubqp_t h, int64_t m) {
     if (m <= h->asc_cap) return UBQP_OK;
-    dfree(h->asc_f); dfree(h->asc_flips); dfree(h->asc_bits); dfree(h->asc_slots);
+    dfree(h->asc_f); dfree(h->asc_flips); dfree(h->asc_bits); dfree(h->asc_slots); dfree(h->asc_aux);
     int64_t cap = m;
     if (cudaMalloc(&h->asc_f, cap * sizeof(int64_t)) != cudaSuccess ||
         cudaMalloc(&h->asc_flips, cap * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->asc_aux, cap * sizeof(int32_t)) != cudaSuccess ||
         cudaMalloc(&h->asc_bits, cap * h->W64 * sizeof(uint64_t)) != cudaSuccess ||
         cudaMalloc(&h->asc_slots, cap * sizeof(int32_t)) != cudaSuccess) {
         cudaGetLastError();
@@ -144,6 +145,27 @@ int ensure_asc(ubqp_t h, int64_t m) {
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate ascent buffers");
     }
     h->asc_cap = cap;
+    return UBQP_OK;
+}
+
+// stage rows*W64 packed words on the device (device pointers pass through)
+int stage_rows(ubqp_t h, const uint64_t *src, int64_t rows, uint64_t *&buf, int64_t &cap, const uint64_t *&out) {
+    if (is_device_ptr(src)) {
+        out = src;
+        return UBQP_OK;
+    }
+    if (rows > cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(buf);
+        cap = 0;
+        if (cudaMalloc(&buf, rows * h->W64 * sizeof(uint64_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate a staging buffer");
+        }
+        cap = rows;
+    }
+    CK(cudaMemcpyAsync(buf, src, rows * h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+    out = buf;
     return UBQP_OK;
 }
 
@@ -272,6 +294,8 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
             q8[static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(Qh[static_cast<int64_t>(i) * n + j]);
         dg[i] = Qh[static_cast<int64_t>(i) * n + i];
     }
+    int qmax = 0;
+    for (int64_t e = 0; e < nn; ++e) qmax = std::max(qmax, std::abs(Qh[e]));
     if (cudaMalloc(&h->Q8, q8.size()) != cudaSuccess || cudaMalloc(&h->diag, dg.size() * 4) != cudaSuccess ||
         cudaMalloc(&h->Q8L, q8l.size()) != cudaSuccess ||
         cudaMalloc(&h->seed, h->W64 * sizeof(uint64_t)) != cudaSuccess) {
@@ -283,6 +307,7 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     CK(cudaMemcpy(h->Q8L, q8l.data(), q8l.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->diag, dg.data(), dg.size() * 4, cudaMemcpyHostToDevice));
     // batch workspace
+    h->qmax = qmax;
     h->k_max = k_max;
     h->k_cap_pad = (k_max + ubqp::kBM - 1) / ubqp::kBM * ubqp::kBM;
     const int64_t nblk = (k_max + 4095) / 4096 + 1;
@@ -343,22 +368,9 @@ int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int
         CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
         seed_dev = h->seed;
     }
-    const uint64_t *par_dev = parents;
-    if (!is_device_ptr(parents)) {
-        if (n_parents > h->parents_cap) {
-            CK(cudaStreamSynchronize(h->stream));
-            dfree(h->parents);
-            h->parents_cap = 0;
-            if (cudaMalloc(&h->parents, n_parents * h->W64 * sizeof(uint64_t)) != cudaSuccess) {
-                cudaGetLastError();
-                return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the parents buffer");
-            }
-            h->parents_cap = n_parents;
-        }
-        CK(cudaMemcpyAsync(h->parents, parents, n_parents * h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                           h->stream));
-        par_dev = h->parents;
-    }
+    const uint64_t *par_dev = nullptr;
+    rc = stage_rows(h, parents, n_parents, h->parents, h->parents_cap, par_dev);
+    if (rc) return rc;
     h->rank = rank;
     h->world = world;
     h->k_local = k_local;
@@ -553,6 +565,62 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, in
     if (!fl_dev && flips_out) {
         for (int64_t i = 0; i < m; ++i)
             if (flips_out[i] < 0) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+    }
+    return UBQP_OK;
+}
+
+int ubqp_relink(ubqp_t h, const uint64_t *guides, int64_t n_guides, const int32_t *slots, int64_t m,
+                int64_t *f_out, int32_t *step_out, int32_t *len_out, uint64_t *bits_out, int64_t *best_key_out) {
+    GUARD(h);
+    if (h->real) return fail(h, UBQP_E_STATE, "ubqp: path relinking runs on integer Q only");
+    if (!h->f_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated batch");
+    if (m < 0 || m > h->k_local || (!slots && m > 0) || !guides || n_guides < 1 || n_guides > (1ll << 22))
+        return fail(h, UBQP_E_INVALID, "ubqp: bad relink arguments");
+    if ((2ll * h->n - 1) * h->qmax >= (1ll << 21))
+        return fail(h, UBQP_E_RANGE, "ubqp: relinking needs (2n-1)*qmax < 2^21");
+    if (!h->gains_valid) {
+        int rc = run_eval(h, true);
+        if (rc) return rc;
+    }
+    int rc = ensure_asc(h, m > 0 ? m : 1);
+    if (rc) return rc;
+    const uint64_t *g_dev = nullptr;
+    rc = stage_rows(h, guides, n_guides, h->guides, h->guides_cap, g_dev);
+    if (rc) return rc;
+    const int32_t *slots_dev = slots;
+    if (m > 0 && !is_device_ptr(slots)) {
+        for (int64_t i = 0; i < m; ++i)
+            if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        slots_dev = h->asc_slots;
+    }
+    const bool f_dev = f_out && is_device_ptr(f_out);
+    const bool s_dev = step_out && is_device_ptr(step_out);
+    const bool l_dev = len_out && is_device_ptr(len_out);
+    const bool b_dev = bits_out && is_device_ptr(bits_out);
+    const bool k_dev = best_key_out && is_device_ptr(best_key_out);
+    int64_t *f_d = f_dev ? f_out : h->asc_f;
+    int32_t *s_d = s_dev ? step_out : h->asc_aux;
+    int32_t *l_d = l_dev ? len_out : h->asc_flips;
+    uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
+    int64_t *k_d = k_dev ? best_key_out : h->scratch64 + 5;
+    CK(cudaMemsetAsync(k_d, 0xFF, sizeof(int64_t), h->stream));     // -1 = none
+    if (ubqp::launch_relink(*h, slots_dev, m, g_dev, n_guides, f_d, nullptr, s_d, l_d, b_d, k_d))
+        return fail(h, UBQP_E_RANGE, "ubqp: n outside the ascent kernel range");
+    CK_LAUNCH("ascend_kernel<relink>");
+    bool sync = false;
+    if (f_out && !f_dev && m) { CK(cudaMemcpyAsync(f_out, f_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (step_out && !s_dev && m) { CK(cudaMemcpyAsync(step_out, s_d, m * 4, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (len_out && !l_dev && m) { CK(cudaMemcpyAsync(len_out, l_d, m * 4, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (bits_out && !b_dev && m) {
+        CK(cudaMemcpyAsync(bits_out, b_d, m * h->W64 * 8, cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
+    }
+    if (best_key_out && !k_dev) { CK(cudaMemcpyAsync(best_key_out, k_d, 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (sync) CK(cudaStreamSynchronize(h->stream));
+    if (!l_dev && len_out) {
+        for (int64_t i = 0; i < m; ++i)
+            if (len_out[i] < 0) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
     }
     return UBQP_OK;
 }

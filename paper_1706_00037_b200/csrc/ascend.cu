@@ -72,35 +72,51 @@ struct Asc {
 // equals 256(-Delta_old) + 2(127 - li) + x_new, and flip x's byte mask.
 template <int L, int NCH>
 __device__ __forceinline__ void owner_fix(int (&K)[NCH][16], uint32_t (&m)[NCH][4],
-                                          const uint4 (&w)[NCH], int gv, int x_new) {
+                                          const uint4 (&w)[NCH], int gv, int x_new, int off) {
     constexpr int c = L >> 4, e = L & 15, wi = e >> 2, b = e & 3;
     if constexpr (c < NCH) {
         const int qkk = sext_byte(word_of(w[c], wi), sel_of(b));
-        K[c][e] = -gv * 256 + 2 * (127 - L) + x_new + 512 * qkk;
+        K[c][e] = -gv * 256 + 2 * (127 - L) + x_new + 512 * qkk - off;
         m[c][wi] ^= 0xFFu << (8 * b);
     }
 }
 
 #define UBQP_CASE(L) \
     case L:          \
-        owner_fix<L, NCH>(K, m, w, gv, x_new); \
+        owner_fix<L, NCH>(K, m, w, gv, x_new, kfix); \
         break;
 #define UBQP_CASE8(B) UBQP_CASE(B) UBQP_CASE(B + 1) UBQP_CASE(B + 2) UBQP_CASE(B + 3) \
                       UBQP_CASE(B + 4) UBQP_CASE(B + 5) UBQP_CASE(B + 6) UBQP_CASE(B + 7)
 
-template <int BLOCK, int NCH, int MINB, bool FULL>
+// Path relinking (O11, NEXT-4; R19) reuses the ascent loop: variables outside
+// D = {j : x_j != y_j} carry keys lowered by kOff = 2^30, below every key in D while
+// (2n-1) qmax < 2^21 (checked by ubqp_relink), so the same argmax walks D in gain order
+// and the flipped variable leaves D through the owner fix.  The walk takes |D| forced steps
+// (moves may worsen f), records the flip order in shared memory and keeps the best strictly
+// interior point, rebuilt at the end as x0 xor (first s_best flips).
+constexpr int kOff = 1 << 30;
+struct RelinkArgs {
+    const uint64_t *guides = nullptr;   // [n_guides][W64]; guide of list entry i: i mod n_guides
+    int64_t n_guides = 0;
+    int32_t *sbest = nullptr;           // [m] step of the best interior point (-1: none)
+    int32_t *len = nullptr;             // [m] |D|
+};
+
+template <int BLOCK, int NCH, int MINB, bool FULL, bool RELINK>
 __global__ void __launch_bounds__(BLOCK, MINB)
 ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int q_ld, int W64,
               int64_t k_local, int rank, int world, const int8_t *__restrict__ Q8,
               const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
               const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out,
               int32_t *__restrict__ flips_out, uint64_t *__restrict__ bits_out,
-              long long *__restrict__ best_key) {
+              long long *__restrict__ best_key, const RelinkArgs rl) {
     using A = Asc<BLOCK, NCH>;
     static_assert(A::E <= 128, "local index must fit 7 bits");
     __shared__ int s_val[2][A::NW];
     __shared__ unsigned s_key[2][A::NW];
     __shared__ uint32_t s_bits[(A::CHUNK * NCH) / 32];
+    __shared__ int s_nd;
+    extern __shared__ uint16_t s_seq[];        // RELINK: flip order (n_pad entries)
 
     const int i = blockIdx.x;
     const int t = threadIdx.x;
@@ -110,6 +126,10 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         if (t == 0) {
             if (flips_out) flips_out[i] = -1;
             if (f_out) f_out[i] = 0;
+            if constexpr (RELINK) {
+                if (rl.sbest) rl.sbest[i] = -1;
+                if (rl.len) rl.len[i] = -1;
+            }
         }
         return;
     }
@@ -118,11 +138,21 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
     uint32_t m[NCH][4];
     const int32_t *grow = gains + s * n_pad;
     const uint64_t *xrow = Xb + s * W64;
+    const uint64_t *yrow = RELINK ? rl.guides + (i % rl.n_guides) * W64 : nullptr;
+    int nd_local = 0;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         const int j0 = c * A::CHUNK + 16 * t;
-        uint32_t bits16 = 0;
+        uint32_t bits16 = 0, out16 = 0;        // out16: variables outside D (relinking)
         if (j0 < n) bits16 = static_cast<uint32_t>(xrow[j0 >> 6] >> (j0 & 63)) & 0xFFFFu;
+        if constexpr (RELINK) {
+            if (j0 < n) {
+                const uint32_t d16 = (bits16 ^ static_cast<uint32_t>(yrow[j0 >> 6] >> (j0 & 63))) & 0xFFFFu &
+                                     (n - j0 >= 16 ? 0xFFFFu : ((1u << (n - j0)) - 1u));
+                nd_local += __popc(d16);
+                out16 = ~d16 & 0xFFFFu;
+            }
+        }
 #pragma unroll
         for (int wi = 0; wi < 4; ++wi) m[c][wi] = byte_mask_of_nibble((bits16 >> (4 * wi)) & 15u);
 #pragma unroll
@@ -134,10 +164,19 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
             for (int b = 0; b < 4; ++b) {
                 const int e = 4 * q4 + b;
                 const int li = 16 * c + e;
-                K[c][e] = (j0 + e < n) ? gg[b] * 256 + 2 * (127 - li) + static_cast<int>((bits16 >> e) & 1u)
+                K[c][e] = (j0 + e < n) ? gg[b] * 256 + 2 * (127 - li) + static_cast<int>((bits16 >> e) & 1u) -
+                                             (RELINK && ((out16 >> e) & 1u) ? kOff : 0)
                                        : kPad;
             }
         }
+    }
+    int nd = 0;
+    if constexpr (RELINK) {
+        if (t == 0) s_nd = 0;
+        __syncthreads();
+        if (nd_local) atomicAdd(&s_nd, nd_local);
+        __syncthreads();
+        nd = s_nd;
     }
     int run = kPad;
 #pragma unroll
@@ -152,6 +191,8 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
     int64_t fv = f_in[s];
     int flips = 0;
     int par = 0;
+    long long best_f = LLONG_MIN;              // RELINK: best strictly interior point
+    int best_s = -1;
     for (;;) {
         // ---- argmax: lane -> warp (max Delta, then min j) -> block
         const int dv = run >> 8;
@@ -184,7 +225,11 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
             }
             par ^= 1;
         }
-        if (gv <= 0 || flips == max_flips) break;
+        if constexpr (RELINK) {
+            if (flips == nd) break;
+        } else {
+            if (gv <= 0 || flips == max_flips) break;
+        }
 
         // ---- flip k*
         const int kstar = static_cast<int>(gk >> 1);
@@ -192,6 +237,14 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         const int C = xk ? -512 : 512;          // 512 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;
+        if constexpr (RELINK) {
+            if (t == 0) s_seq[flips - 1] = static_cast<uint16_t>(kstar);
+            if (flips < nd && fv > best_f) {
+                best_f = fv;
+                best_s = flips;
+            }
+        }
+        constexpr int kfix = RELINK ? kOff : 0;   // k* leaves D
         const uint4 *qrow = reinterpret_cast<const uint4 *>(qbase + static_cast<int64_t>(kstar) * q_ld);
         uint4 w[NCH];
 #pragma unroll
@@ -246,6 +299,40 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
     }
 
     // ---- outputs
+    if constexpr (RELINK) {
+        // x at the best interior step: x0 xor the first best_s flips
+        __syncthreads();
+        if (bits_out) {
+            for (int w2 = t; w2 < W64; w2 += BLOCK) {
+                const uint64_t x0w = xrow[w2];
+                s_bits[2 * w2] = static_cast<uint32_t>(x0w);
+                s_bits[2 * w2 + 1] = static_cast<uint32_t>(x0w >> 32);
+            }
+            __syncthreads();
+            for (int f2 = t; f2 < best_s; f2 += BLOCK) {
+                const int j = s_seq[f2];
+                atomicXor(&s_bits[j >> 5], 1u << (j & 31));
+            }
+            __syncthreads();
+            for (int w2 = t; w2 < W64; w2 += BLOCK)
+                bits_out[static_cast<int64_t>(i) * W64 + w2] =
+                    static_cast<uint64_t>(s_bits[2 * w2]) | (static_cast<uint64_t>(s_bits[2 * w2 + 1]) << 32);
+        }
+        if (t == 0) {
+            if (f_out) f_out[i] = best_f;
+            if (flips_out) flips_out[i] = flips;
+            if (rl.sbest) rl.sbest[i] = best_s;
+            if (rl.len) rl.len[i] = nd;
+            if (best_key && best_s >= 0) {
+                const int64_t g = static_cast<int64_t>(rank) + s * world;
+                const long long key = static_cast<long long>(
+                    (static_cast<uint64_t>(best_f + (1ll << 40)) << 22) |
+                    static_cast<uint64_t>((1ll << 22) - 1 - g));
+                atomicMax(best_key, key);
+            }
+        }
+        return;
+    }
     if (bits_out) {
         for (int w2 = t; w2 < (A::CHUNK * NCH) / 32; w2 += BLOCK) s_bits[w2] = 0;
         __syncthreads();
@@ -279,20 +366,34 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
 
 template <int BLOCK, int NCH>
 void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_dev,
-                 int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
+                 int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev, const RelinkArgs *rl) {
     const bool full = 16 * BLOCK * NCH <= c.q_ld;
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
     // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
     constexpr int kRegs = NCH >= 5 ? 170 : 24 * NCH + 48;   // 170: 6 CTAs of 64 threads per SM (small spills at NCH = 7, measured faster)
     constexpr int kMinBlocks = (65536 / (BLOCK * kRegs)) < 1 ? 1 : 65536 / (BLOCK * kRegs);
+    long long *bk = reinterpret_cast<long long *>(best_dev);
+    const unsigned grid = static_cast<unsigned>(m);
+    if (rl) {
+        const size_t seq = static_cast<size_t>(c.n_pad) * sizeof(uint16_t);
+        if (full)
+            ascend_kernel<BLOCK, NCH, kMinBlocks, true, true><<<grid, BLOCK, seq, c.stream>>>(
+                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+                c.Xb, f_dev, flips_dev, bits_dev, bk, *rl);
+        else
+            ascend_kernel<BLOCK, NCH, kMinBlocks, false, true><<<grid, BLOCK, seq, c.stream>>>(
+                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+                c.Xb, f_dev, flips_dev, bits_dev, bk, *rl);
+        return;
+    }
     if (full)
-        ascend_kernel<BLOCK, NCH, kMinBlocks, true><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
+        ascend_kernel<BLOCK, NCH, kMinBlocks, true, false><<<grid, BLOCK, 0, c.stream>>>(
             slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
-            c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
+            c.Xb, f_dev, flips_dev, bits_dev, bk, RelinkArgs{});
     else
-        ascend_kernel<BLOCK, NCH, kMinBlocks, false><<<static_cast<unsigned>(m), BLOCK, 0, c.stream>>>(
+        ascend_kernel<BLOCK, NCH, kMinBlocks, false, false><<<grid, BLOCK, 0, c.stream>>>(
             slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
-            c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev));
+            c.Xb, f_dev, flips_dev, bits_dev, bk, RelinkArgs{});
 }
 
 }  // namespace
@@ -326,8 +427,8 @@ int ascend_capacity(int n_pad) {
     return 16 * b * nch;
 }
 
-int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
-                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
+static int launch_walk(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
+                       int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev, const RelinkArgs *rl) {
     if (m <= 0) return 0;
     const int np = c.n_pad;
     int fb = 0, fn = 0;
@@ -339,7 +440,7 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
     if (!fb) { fb = db; fn = dn; }
 #define UBQP_ASC(B, N)                                                                          \
     if (fb == B && fn == N) {                                                                   \
-        launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);    \
+        launch_inst<B, N>(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev, rl); \
         ++c.launches;                                                                           \
         return 0;                                                                               \
     }
@@ -355,6 +456,22 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
 #undef UBQP_ASC_ALL
 #undef UBQP_ASC
     return 1;
+}
+
+int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
+                  int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
+    return launch_walk(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev, nullptr);
+}
+
+int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
+                  int64_t *f_dev, int32_t *steps_dev, int32_t *sbest_dev, int32_t *len_dev, uint64_t *bits_dev,
+                  int64_t *best_dev) {
+    RelinkArgs rl;
+    rl.guides = guides_dev;
+    rl.n_guides = n_guides;
+    rl.sbest = sbest_dev;
+    rl.len = len_dev;
+    return launch_walk(c, slots_dev, m, 0, f_dev, steps_dev, bits_dev, best_dev, &rl);
 }
 
 }  // namespace ubqp

@@ -35,9 +35,12 @@ struct Ctx {
     int q_ld = 0;                // Q8 row stride >= n_pad: the ascent's register capacity (zero tail)
     int8_t *Q8 = nullptr;        // [q_rows][q_ld] row-major, zero padded; row k = column k (Q = Q^t)
     int32_t *diag = nullptr;     // [q_rows]
+    int qmax = 0;                // max |Q_ij| of the loaded integer Q
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
     int64_t parents_cap = 0;
+    uint64_t *guides = nullptr;  // [guides_cap][W64] staged relinking guides (host callers)
+    int64_t guides_cap = 0;
     // batch workspace
     int64_t k_max = 0, k_cap_pad = 0, k_local = -1;
     int rank = 0, world = 1;
@@ -51,7 +54,7 @@ struct Ctx {
     int64_t *scratch64 = nullptr;// small device scratch (stats, m, best key)
     // ascent outputs scratch
     int64_t *asc_f = nullptr; int32_t *asc_flips = nullptr; uint64_t *asc_bits = nullptr;
-    int32_t *asc_slots = nullptr; int64_t asc_cap = 0;
+    int32_t *asc_slots = nullptr; int32_t *asc_aux = nullptr; int64_t asc_cap = 0;
     // TMA descriptors (64 B each, passed by value as __grid_constant__)
     CUtensorMap tmap_X8{}, tmap_Q8{};
     int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
@@ -95,6 +98,10 @@ void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
 int ascend_capacity(int n_pad);   // variables covered by the default ascent shape (>= n_pad)
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,
                   int64_t *f_dev, int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
+// path relinking (O11) of batch slots toward guides[i mod n_guides] on the ascent kernel
+int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
+                  int64_t *f_dev, int32_t *steps_dev, int32_t *sbest_dev, int32_t *len_dev, uint64_t *bits_dev,
+                  int64_t *best_dev);
 
 }  // namespace ubqp
 

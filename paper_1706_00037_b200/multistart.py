@@ -21,6 +21,7 @@ from .ubqp import UBQP_EMIT_GAINS, Ubqp
 
 KEY_SHIFT = 22
 F_OFFSET = 1 << 40
+POLISH_MAX_PAIRS = 72            # E (E - 1) for an elite set of pool_cap + 1 = 9
 
 
 def key_f(key: int) -> int:
@@ -120,10 +121,11 @@ class MultiStart:
         self.stream = torch.cuda.Stream(device=self.device)
         torch.cuda.set_stream(self.stream)
         self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
-        self.u.load_Q(np.ascontiguousarray(Q, dtype=np.int32), max(self.k_local, 1))
+        # workspace also holds a polish batch: all ordered pairs of <= 9 elite solutions
+        self.u.load_Q(np.ascontiguousarray(Q, dtype=np.int32), max(self.k_local, POLISH_MAX_PAIRS))
         self.W64 = self.u.W64
         dv = torch.device("cuda", self.device)
-        kl = max(self.k_local, 1)
+        kl = max(self.k_local, POLISH_MAX_PAIRS)
         self.stats = torch.zeros(4, dtype=torch.int64, device=dv)
         self.surv = torch.zeros(kl, dtype=torch.int32, device=dv)
         self.f_asc = torch.zeros(kl, dtype=torch.int64, device=dv)
@@ -184,14 +186,52 @@ class MultiStart:
             best_bits = self.bits[i].clone()
         return RoundResult(m, T, best_key, best_bits, batch_max, mean_sum, mean_count)
 
+    def polish(self, elite: torch.Tensor):
+        """Path relinking over an elite set (NEXT-4, R19): every ordered pair (a, b), a != b,
+        relinked from elite[a] toward elite[b] (ubqp_relink), the best interior points
+        ascended (ubqp_ascend).  Replicated on every rank (a few dozen walks), so the result
+        is the same for any world size.  Returns (f, bits) or None."""
+        E = int(elite.shape[0])
+        pairs = [(a, b) for a in range(E) for b in range(E) if a != b]
+        if not pairs:
+            return None
+        if len(pairs) > POLISH_MAX_PAIRS:
+            raise ValueError(f"polish: at most {POLISH_MAX_PAIRS} pairs")
+        dv = elite.device
+        ia = torch.tensor([a for a, _ in pairs], device=dv)
+        ib = torch.tensor([b for _, b in pairs], device=dv)
+        X0 = elite[ia].contiguous()
+        Y = elite[ib].contiguous()
+        m = len(pairs)
+        u = self.u
+        u.set_batch(X0, m, 0, 1)
+        u.eval_batch(UBQP_EMIT_GAINS)
+        slots = torch.arange(m, dtype=torch.int32, device=dv)
+        f = torch.zeros(m, dtype=torch.int64, device=dv)
+        st = torch.zeros(m, dtype=torch.int32, device=dv)
+        bits = torch.zeros((m, self.W64), dtype=torch.int64, device=dv)
+        u.relink(Y, m, slots, m, f, st, None, bits, None)
+        sel = torch.nonzero(st >= 0).flatten()
+        k = int(sel.numel())
+        if k == 0:
+            return None
+        u.set_batch(bits[sel].contiguous(), k, 0, 1)
+        u.eval_batch(UBQP_EMIT_GAINS)
+        u.ascend(slots[:k], k, self.max_flips, self.f_asc, self.flips, self.bits, self.key)
+        key = int(self.key.item())
+        i = key_g(key)
+        return key_f(key), self.bits[i].clone()
+
     def run(self, rounds: int, sample_seed: int, t_start: int = 0, lam_policy: str = "fixed",
-            div: str = "glover", pool_cap: int = 8):
+            div: str = "glover", pool_cap: int = 8, polish_end: bool = False):
         """Figure 2 as batched rounds (O8): pinned sampling mean, first-derivative
         incumbent, rounds of diversify/eval/screen/ascend; strict improvement.
         lam_policy "paper": lambda = Max/Mean = Starting_solution/Mean, clamped to
         (0, 1] with 0.5 when Mean <= 0 or the start's value <= 0 (R7).
         div "blend": once the parent pool is non-empty, rounds blend the incumbent with
-        pool[g mod P] (O4b) instead of Glover's generator."""
+        pool[g mod P] (O4b) instead of Glover's generator.  polish_end: after the
+        last round, polish(pool + [incumbent]); a strict improvement is recorded as round
+        rounds + 1."""
         mean = self.sample_mean(sample_seed)
         inc_bits, inc_f = self.first_derivative()
         if lam_policy == "paper":
@@ -207,7 +247,12 @@ class MultiStart:
                 inc_f = key_f(res.best_key)
                 inc_bits = res.best_bits.clone()
                 traj.append((r, inc_f))
-            if div == "blend":
+            if div == "blend" or polish_end:
                 pool = pool_update(pool, pool_cap, inc_bits, improved_from,
                                    res.best_bits if res.best_key >= 0 else None)
+        if polish_end:
+            res = self.polish(torch.stack(pool + [inc_bits]))
+            if res is not None and res[0] > inc_f:
+                inc_f, inc_bits = res
+                traj.append((rounds + 1, inc_f))
         return inc_f, inc_bits, traj

@@ -23,7 +23,7 @@ Q_N, Q_NPAD, Q_W64, Q_KMAX, Q_KLOCAL, Q_LAUNCHES, Q_STREAM = range(7)
 # every entry point declared in include/ubqp.h
 EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ubqp_load_Q",
            "ubqp_diversify", "ubqp_blend", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
-           "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_sync", "ubqp_query",
+           "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_relink", "ubqp_sync", "ubqp_query",
            "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real"]
 UBQP_F32, UBQP_F64 = 1, 2
 Q_REAL_EXP, Q_IS_REAL = 7, 8
@@ -76,6 +76,7 @@ def load_library(path: Path | str | None = None):
         "ubqp_get_gains": ([P, i64, i64, P], ctypes.c_int),
         "ubqp_screen": ([P, dbl, i64, i64, i64, P, P, P], ctypes.c_int),
         "ubqp_ascend": ([P, P, i64, i32, P, P, P, P], ctypes.c_int),
+        "ubqp_relink": ([P, P, i64, P, i64, P, P, P, P, P], ctypes.c_int),
         "ubqp_sync": ([P], ctypes.c_int),
         "ubqp_query": ([P, ctypes.c_int, ctypes.POINTER(i64)], ctypes.c_int),
         "ubqp_load_Q_real": ([P, i32, ctypes.c_int, P, i64], ctypes.c_int),
@@ -189,6 +190,11 @@ class Ubqp:
                best_key_out=None):
         self._ck(self.lib.ubqp_ascend(self.h, _ptr(slots), m, max_flips, _ptr(f_out), _ptr(flips_out),
                                       _ptr(bits_out), _ptr(best_key_out)))
+
+    def relink(self, guides, n_guides: int, slots, m: int, f_out=None, step_out=None, len_out=None,
+               bits_out=None, best_key_out=None):
+        self._ck(self.lib.ubqp_relink(self.h, _ptr(guides), n_guides, _ptr(slots), m, _ptr(f_out),
+                                      _ptr(step_out), _ptr(len_out), _ptr(bits_out), _ptr(best_key_out)))
 
     # ---- real-valued Q (a4')
     def load_Q_real(self, Q, k_max: int):

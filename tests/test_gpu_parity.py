@@ -348,6 +348,59 @@ def test_multistart_rounds_match_oracle(n, K, rounds, lam):
     assert np.array_equal(got, ox)
 
 
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 64, 65, 129, 500, 1100, 2500])
+def test_relink_matches_oracle(n):
+    """O11 path relinking (NEXT-4, R19) bit-exact: best interior value, its step, |D|, the
+    interior solution and the best key; host and device guides, several guides."""
+    Q = generate_Q(n, 0.5, seed=300 + n)
+    rng = np.random.default_rng(n)
+    K = 150
+    X0 = rng.integers(0, 2, size=(K, n)).astype(np.uint8)
+    G = rng.integers(0, 2, size=(3, n)).astype(np.uint8)
+    slots = np.arange(K, dtype=np.int32)[::-1].copy()   # list order differs from slot order
+    X0[slots[3]] = G[0]                             # list entry 3 -> guide 0: |D| = 0
+    X0[slots[4]] = G[1]
+    X0[slots[4]][0] ^= 1                            # list entry 4 -> guide 1: |D| = 1
+    u = _handle_with(Q, K)
+    u.set_batch(pack_bits(X0), K)
+    f0 = np.zeros(K, np.int64)
+    u.eval_batch(UBQP_EMIT_GAINS, f0)
+    Xs = X0[slots]
+    ob, of, os_, ol = oracle.relink(Q, Xs, f0[slots], G, nthreads=8)
+    for guides in (pack_bits(G), torch.from_numpy(pack_bits(G).view(np.int64)).cuda()):
+        f = np.zeros(K, np.int64)
+        st = np.zeros(K, np.int32)
+        ln = np.zeros(K, np.int32)
+        b = np.zeros((K, u.W64), np.uint64)
+        key = np.zeros(1, np.int64)
+        u.relink(guides, 3, slots, K, f, st, ln, b, key)
+        assert np.array_equal(ln, ol) and np.array_equal(st, os_) and np.array_equal(f, of)
+        assert np.array_equal(unpack_bits(b, n), ob)
+        has = os_ >= 0
+        want = max((oracle.max_key(int(of[i]), int(slots[i])) for i in np.flatnonzero(has)), default=-1)
+        assert int(key[0]) == want
+
+
+def test_relink_range_and_errors():
+    n = 9000                                        # (2n-1)*qmax >= 2^21 at qmax = 127
+    Q = np.zeros((n, n), np.int32)
+    Q[0, 0] = 127
+    u = _handle_with(Q, 4)
+    u.random(1, 4)
+    u.eval_batch(UBQP_EMIT_GAINS)
+    g = np.zeros((1, u.W64), np.uint64)
+    with pytest.raises(UbqpError):
+        u.relink(g, 1, np.arange(4, dtype=np.int32), 4)
+    Q2 = generate_Q(100, 0.5, seed=1)
+    u2 = _handle_with(Q2, 4)
+    u2.random(1, 4)
+    u2.eval_batch(UBQP_EMIT_GAINS)
+    with pytest.raises(UbqpError):
+        u2.relink(np.zeros((1, u2.W64), np.uint64), 0, np.arange(4, dtype=np.int32), 4)
+    with pytest.raises(UbqpError):
+        u2.relink(np.zeros((1, u2.W64), np.uint64), 1, np.array([0, 9], np.int32), 2)
+
+
 @pytest.mark.parametrize("n", [1, 2, 200, 257, 513, 2500])
 def test_symmetric_and_full_eval_agree(n, monkeypatch):
     """f-only evaluations use the triangular GEMM (NEXT-1); UBQP_FULL_EVAL=1 forces the full
@@ -439,6 +492,32 @@ def test_multistart_blend_matches_oracle(n, K, rounds, lam):
     ms = MultiStart(Q, K, lam=lam, max_flips=10 * n)
     best, bits, traj = ms.run(rounds, sample_seed=4, div="blend")
     obest, ox, otraj = oracle.run_rounds(Q, K, rounds, lam, 10 * n, sample_seed=4, nthreads=8, div="blend")
+    assert best == obest and traj == otraj
+    assert np.array_equal(unpack_bits(bits.cpu().numpy().view(np.uint64), n)[0], ox)
+
+
+@pytest.mark.parametrize("n,E", [(40, 4), (700, 9), (2500, 5)])
+def test_polish_matches_oracle(n, E):
+    from paper_1706_00037_b200.multistart import MultiStart
+    Q = generate_Q(n, 0.5, seed=400 + n)
+    rng = np.random.default_rng(n)
+    El = rng.integers(0, 2, size=(E, n)).astype(np.uint8)
+    El[1] = El[0]                                   # a pair with |D| = 0 both ways
+    ms = MultiStart(Q, 64, lam=0.5, max_flips=10 * n)
+    got = ms.polish(torch.from_numpy(pack_bits(El).view(np.int64)).cuda())
+    want = oracle.polish(Q, El, 10 * n, nthreads=8)
+    assert got[0] == want[0]
+    assert np.array_equal(unpack_bits(got[1].cpu().numpy().view(np.uint64)[None, :], n)[0], want[1])
+
+
+@pytest.mark.parametrize("n,K,rounds,div", [(60, 400, 4, "glover"), (300, 1500, 3, "blend")])
+def test_multistart_polish_matches_oracle(n, K, rounds, div):
+    from paper_1706_00037_b200.multistart import MultiStart
+    Q = generate_Q(n, 0.5, seed=500 + n)
+    ms = MultiStart(Q, K, lam=0.4, max_flips=10 * n)
+    best, bits, traj = ms.run(rounds, sample_seed=6, div=div, polish_end=True)
+    obest, ox, otraj = oracle.run_rounds(Q, K, rounds, 0.4, 10 * n, sample_seed=6, nthreads=8, div=div,
+                                         polish_end=True)
     assert best == obest and traj == otraj
     assert np.array_equal(unpack_bits(bits.cpu().numpy().view(np.uint64), n)[0], ox)
 
