@@ -345,6 +345,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["real_q_eval"] = real_q_eval(local_rank)
         out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
         out["ascent_microbench"] = ascent_microbench(local_rank)
+        out["relink_microbench"] = relink_microbench(local_rank)
     print(json.dumps(out), flush=True)
 
 
@@ -481,6 +482,38 @@ def ascent_microbench(device):
                         "TB_per_s_qrow": steps * n / (ms * 1e-3) / 1e12}
         u.close()
     return out
+
+
+def relink_microbench(device):
+    """NEXT-4 path relinking (O11): m = 8192 random starts (SplitMix64 seed 5) relinked
+    toward 8 random guides (seed 6, i mod 8) at n = 7000 dense: |D| ~ n/2 forced steps
+    each, the same per-step work as the ascent (one Q row of n bytes)."""
+    import torch
+
+    from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp
+    n, m = 7000, 8192
+    Q = generate_Q(n, 1.0, seed=5)
+    u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+    u.load_Q(Q, m)
+    u.random(6, 8)
+    guides = torch.zeros((8, u.W64), dtype=torch.int64, device="cuda")
+    u.get_batch(guides)
+    u.random(5, m)
+    u.eval_batch(UBQP_EMIT_GAINS)
+    slots = torch.arange(m, dtype=torch.int32, device="cuda")
+    ln = torch.zeros(m, dtype=torch.int32, device="cuda")
+    fo = torch.zeros(m, dtype=torch.int64, device="cuda")
+    u.relink(guides, 8, slots, m, fo, None, ln)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    u.relink(guides, 8, slots, m, fo, None, ln)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    steps = int(ln.sum().item())
+    u.close()
+    return {"n": n, "m": m, "ms": ms, "steps": steps, "steps_per_s": steps / (ms * 1e-3),
+            "TB_per_s_qrow": steps * n / (ms * 1e-3) / 1e12}
 
 
 def real_q_eval(device):
