@@ -353,6 +353,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["cpu_baseline"] = cpu_baseline(cfg, Q)
     if world == 1 and not args.no_table1:
         out["table1_eval_1000"] = table1_eval(local_rank)
+        out["config1_round"] = config1_round(local_rank)
         out["real_q_eval"] = real_q_eval(local_rank)
         out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
         out["ascent_microbench"] = ascent_microbench(local_rank)
@@ -406,6 +407,34 @@ def cpu_baseline(cfg, Q):
     return {"value": S / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {S} of the {cfg['K']} Glover solutions (eval + screen + ascent of {m} "
                       f"survivors, {fl} flips), {cores} threads, {dt:.1f} s"}
+
+
+def config1_round(device):
+    """SURVEY §8(d) config 1 (n = 50, density 0.1, K = 1000 Glover solutions from the
+    first-derivative seed, lambda = 0.5, max_flips = 500): the whole round, latency-bound
+    (everything on-chip).  Reports evals/s and ascent steps/s, no roofline %."""
+    import torch
+
+    from paper_1706_00037_b200.multistart import MultiStart
+    cfg = CONFIGS[1]
+    Q = generate_Q(cfg["n"], cfg["density"], seed=cfg["seed_Q"])
+    ms = MultiStart(Q, cfg["K"], lam=cfg["lam"], max_flips=cfg["max_flips"], device=device)
+    x0, f0 = ms.first_derivative()
+    for _ in range(5):
+        ms.round(x0, 0, f0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps, steps = 50, 0
+    e0.record(ms.stream)
+    for _ in range(reps):
+        res = ms.round(x0, 0, f0)
+        steps += int(ms.flips[:res.m].sum().item()) if res.m else 0
+    e1.record(ms.stream)
+    torch.cuda.synchronize()
+    ms_round = e0.elapsed_time(e1) / reps
+    ms.u.close()
+    return {"n": cfg["n"], "K": cfg["K"], "ms_per_round": ms_round, "evals_per_s": cfg["K"] / (ms_round * 1e-3),
+            "ascent_steps_per_round": steps // reps, "note": "round incl. host syncs of screen/best record"}
 
 
 def table1_eval(device):

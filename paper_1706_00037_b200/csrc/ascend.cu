@@ -112,8 +112,9 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
               long long *__restrict__ best_key, const RelinkArgs rl) {
     using A = Asc<BLOCK, NCH>;
     static_assert(A::E <= 128, "local index must fit 7 bits");
-    __shared__ int s_val[2][A::NW];
-    __shared__ unsigned s_key[2][A::NW];
+    // per-warp winners as one orderable word: (Delta + 2^30) << 32 | ~(j << 1 | x), so a
+    // plain unsigned 64-bit max picks the largest gain, then the lowest index
+    __shared__ unsigned long long s_win[2][A::NW];
     __shared__ uint32_t s_bits[(A::CHUNK * NCH) / 32];
     __shared__ int s_nd;
     extern __shared__ uint16_t s_seq[];        // RELINK: flip order (n_pad entries)
@@ -210,19 +211,15 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
             gv = wv;
             gk = wk;
         } else {
-            if (lane == 0) {
-                s_val[par][warp] = wv;
-                s_key[par][warp] = wk;
-            }
+            if (lane == 0)
+                s_win[par][warp] = (static_cast<unsigned long long>(static_cast<unsigned>(wv + (1 << 30))) << 32) |
+                                   static_cast<unsigned long long>(~wk);
             __syncthreads();
-            gv = s_val[par][0];
-            gk = s_key[par][0];
+            unsigned long long best = s_win[par][0];
 #pragma unroll
-            for (int w2 = 1; w2 < A::NW; ++w2) {
-                const int v = s_val[par][w2];
-                const unsigned k2 = s_key[par][w2];
-                if (v > gv || (v == gv && k2 < gk)) { gv = v; gk = k2; }
-            }
+            for (int w2 = 1; w2 < A::NW; ++w2) best = max(best, s_win[par][w2]);
+            gv = static_cast<int>(static_cast<unsigned>(best >> 32)) - (1 << 30);
+            gk = ~static_cast<unsigned>(best);
             par ^= 1;
         }
         if constexpr (RELINK) {
