@@ -8,6 +8,7 @@ raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
@@ -55,7 +56,8 @@ def load_library(path: Path | str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # UBQP_LIB: load another build of the same library (A/B timing of kernel variants)
+    p = Path(path) if path else Path(os.environ.get("UBQP_LIB", LIB_PATH))
     if not p.exists():
         raise OSError(f"{p} not built: run __graft_entry__.build() (no CPU fallback exists)")
     lib = ctypes.CDLL(str(p))
