@@ -22,7 +22,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC,-ffp-contract=off",
     "-cudart", "static",
     "--expt-relaxed-constexpr",
-    "--split-compile=0",
+    # no --split-compile: its parallel partitioning made ptxas output vary between builds
 ]
 
 

@@ -266,9 +266,11 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         // interleave (t_e, m_e) byte pairs and let IDP2A add C t_e - C m_e = C s_e q_e
         // (m_e = -1 where x_e = 1, so the ones' complement is completed exactly).
         const uint32_t a2 = (static_cast<uint32_t>(C) & 0xFFFFu) | (static_cast<uint32_t>(-C) << 16);
-        int r0 = kPad, r1 = kPad, r2 = kPad, r3 = kPad;   // 4 independent max chains
+        int r0 = kPad, r1 = kPad, r2 = kPad, r3 = kPad;   // 8 independent max chains
+        int r4 = kPad, r5 = kPad, r6 = kPad, r7 = kPad;
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
+        for (int cc = 0; cc < NCH; ++cc) {
+            const int c = NCH - 1 - cc;
 #pragma unroll
             for (int wi = 0; wi < 4; ++wi) {
                 const uint32_t mw = m[c][wi];
@@ -283,16 +285,26 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
                 k1 = dp2a_hi(a2, blo, k1);
                 k2 = dp2a_lo(a2, bhi, k2);
                 k3 = dp2a_hi(a2, bhi, k3);
-                if (wi & 1) {
-                    r2 = max(r2, max(k0, k1));
-                    r3 = max(r3, max(k2, k3));
+                if (c & 1) {
+                    if (wi & 1) {
+                        r6 = max(r6, max(k0, k1));
+                        r7 = max(r7, max(k2, k3));
+                    } else {
+                        r4 = max(r4, max(k0, k1));
+                        r5 = max(r5, max(k2, k3));
+                    }
                 } else {
-                    r0 = max(r0, max(k0, k1));
-                    r1 = max(r1, max(k2, k3));
+                    if (wi & 1) {
+                        r2 = max(r2, max(k0, k1));
+                        r3 = max(r3, max(k2, k3));
+                    } else {
+                        r0 = max(r0, max(k0, k1));
+                        r1 = max(r1, max(k2, k3));
+                    }
                 }
             }
         }
-        run = max(max(r0, r1), max(r2, r3));
+        run = max(max(max(r0, r1), max(r2, r3)), max(max(r4, r5), max(r6, r7)));
     }
 
     // ---- outputs
