@@ -379,7 +379,10 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
     const bool full = 16 * BLOCK * NCH <= c.q_ld;
     // register budget ~ 16*NCH keys + 4*NCH masks + 4*NCH loaded words + ~25
     // registers ~ 16*NCH keys + 8*NCH mask/load words + ~30: 168 at NCH = 5
-    constexpr int kRegs = NCH >= 5 ? 170 : 24 * NCH + 48;   // 170: 6 CTAs of 64 threads per SM (small spills at NCH = 7, measured faster)
+    // 170: 6 CTAs of 64 threads per SM for 96-112 keys (small spills at NCH = 7, measured
+    // faster than 5 CTAs); 128 for 80 keys: 8 CTAs, no spills (same-box A/B: n = 5000
+    // 1.09 -> 1.40 Gsteps/s; 96 keys at 128 spill 104 B and lose)
+    constexpr int kRegs = NCH == 5 ? 128 : (NCH >= 6 ? 170 : 24 * NCH + 48);
     constexpr int kMinBlocks = (65536 / (BLOCK * kRegs)) < 1 ? 1 : 65536 / (BLOCK * kRegs);
     long long *bk = reinterpret_cast<long long *>(best_dev);
     const unsigned grid = static_cast<unsigned>(m);
