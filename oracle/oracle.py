@@ -22,6 +22,7 @@ __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
     "first_derivative_start", "relink", "polish", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
+    "real_image", "ascend_real",
 ]
 
 
@@ -347,3 +348,33 @@ def first_derivative_start_real(Q) -> np.ndarray:
     import math
     Q = np.asarray(Q, dtype=np.float64)
     return np.array([1 if math.fsum(row.tolist()) > 0 else 0 for row in Q], dtype=np.uint8)
+
+
+# O9b -- real-Q ascent (reading R20): the walk runs exactly on the load-time
+# fixed-point image Qt = rint(Q 2^e) (round half to even), e the largest integer with
+# max|Q| 2^e <= 2^27 - 1 (the 28-bit range of four balanced base-128 int8 limbs, a4');
+# f = 2^-e f~ with f~ = x^t Qt x.  Written from that definition, independently of the
+# library's load routine.
+def real_image(Q):
+    """(Qt int64 [n][n], e)"""
+    Q = np.asarray(Q, dtype=np.float64)
+    amax = float(np.abs(Q).max()) if Q.size else 0.0
+    e = 0
+    if amax > 0:
+        lim = float(2**27 - 1)
+        e = 0
+        while np.ldexp(amax, e) > lim:
+            e -= 1
+        while np.ldexp(amax, e + 1) <= lim:
+            e += 1
+    return np.rint(np.ldexp(Q, e)).astype(np.int64), e
+
+
+def ascend_real(Q, X, max_flips: int, nthreads: int = 1):
+    """Steepest ascent (O7) on the image Qt of a real Q (R20): returns (X_final, f~ int64,
+    f = 2^-e f~ float64, flips, e)."""
+    Qt, e = real_image(Q)
+    X = np.asarray(X, dtype=np.uint8)
+    f0 = eval_batch(Qt.astype(np.int32), X, nthreads)
+    Xa, fa, fl = ascend(Qt.astype(np.int32), X, f0, max_flips, nthreads)
+    return Xa, fa, np.ldexp(fa.astype(np.float64), -e), fl, e

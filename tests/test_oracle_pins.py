@@ -566,3 +566,37 @@ def test_paper_lambda_policy_spec_examples():
     assert paper_lambda(-0.5, 2) == 0.5
     assert paper_lambda(100.0, 100) == 1.0
     assert paper_lambda(400.0, 100) == 0.25
+
+
+# ---------------------------------------------------------------- O9b real-Q ascent image (R20)
+def test_real_image_scale_rule_and_rounding():
+    def one(v):
+        return np.array([[v]], dtype=np.float64)
+    assert oracle.real_image(one(1.0))[1] == 26          # 2^26 <= 2^27 - 1 < 2^27
+    assert oracle.real_image(one(0.75))[1] == 27         # 0.75 * 2^27 fits, 0.75 * 2^28 does not
+    assert oracle.real_image(one(100.0))[1] == 20        # 100 * 2^20 = 104857600 <= 134217727
+    Qt, e = oracle.real_image(np.array([[2**27 - 1, 2.5], [2.5, 3.5]]))
+    assert e == 0 and Qt.tolist() == [[2**27 - 1, 2], [2, 4]]   # round half to even
+
+
+def test_real_ascent_reduces_to_integer_ascent():
+    # integer-valued real Q with max |Q| = 100: the image is Q * 2^20 exactly, so the walk is
+    # the integer walk and f~ = 2^20 f (ties the reading to the pinned integer oracle)
+    Q = generate_Q(60, 0.5, -100, 100, seed=61).astype(np.int32)
+    Q[0, 0] = 100
+    X = oracle.random_solutions(60, 8, 40)
+    Xa, fa, ff, fl, e = oracle.ascend_real(Q.astype(np.float64), X, 600)
+    Xi, fi, fli = oracle.ascend(Q, X, oracle.eval_batch(Q, X), 600)
+    assert e == 20 and np.array_equal(Xa, Xi) and np.array_equal(fl, fli)
+    assert np.array_equal(fa, fi * 2**20) and np.array_equal(ff, fi.astype(np.float64))
+
+
+def test_real_ascent_value_within_rounding_bound():
+    rng = np.random.default_rng(62)
+    n = 80
+    A = rng.uniform(-100, 100, size=(n, n))
+    Q = np.triu(A) + np.triu(A, 1).T
+    Xa, fa, ff, fl, e = oracle.ascend_real(Q, oracle.random_solutions(n, 9, 20), 800)
+    for x, f in zip(Xa, ff):
+        S = int(x.sum())
+        assert abs(f - oracle.xQx_real(Q, x)) <= S * S * 2.0 ** (-(e + 1)) + 1e-9
