@@ -220,6 +220,19 @@ int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out);
 int ubqp_screen_real(ubqp_t h, double lambda, double mean, double max_value, int32_t *surv_out,
                      int64_t *m_out, double *T_out);
 
+/* Steepest ascent for real-valued Q (reading R20): ubqp_ascend's walk
+ * (gains P:53; k* = argmax Delta, lowest j on ties; stop at Delta_k* <= 0
+ * or max_flips) run exactly in int64 on the load-time fixed-point image
+ * Qt = rint(Q 2^e) (half-even; e = ubqp_query(UBQP_Q_REAL_EXP), the largest integer with
+ * max|Q| 2^e <= 2^27 - 1).  Starts: batch slots slots[i] of the last ubqp_eval_batch_real
+ * (their int64 gains are formed here from the four int8 limb-plane GEMMs).  Outputs per i
+ * (any may be NULL): f_out double[m] = 2^-e f~ (f~ = x^t Qt x of the local optimum, exact),
+ * fint_out int64[m] = f~, flips_out int32[m], bits_out uint64[m][W64].  The batch is not
+ * modified.  Memory: an int64 gains buffer of k_max * n_pad words on first use.
+ * Errors: E_STATE (no real Q / no evaluated real batch), E_INVALID, E_NOMEM, E_RANGE. */
+int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
+                     double *f_out, int64_t *fint_out, int32_t *flips_out, uint64_t *bits_out);
+
 /* Wait for all work queued on the handle's stream. */
 int ubqp_sync(ubqp_t h);
 

@@ -12,7 +12,7 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libubqp.so"
-SOURCES = ["abi.cu", "gen.cu", "eval_tc.cu", "screen.cu", "ascend.cu"]
+SOURCES = ["abi.cu", "gen.cu", "eval_tc.cu", "screen.cu", "ascend.cu", "ascend_real.cu"]
 HEADERS = ["ubqp_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

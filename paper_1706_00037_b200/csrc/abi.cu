@@ -75,7 +75,7 @@ void free_batch(Ctx &c) {
     dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots); dfree(c.asc_aux);
     c.asc_cap = 0;
     c.k_max = 0; c.k_cap_pad = 0; c.k_local = -1;
-    c.f_valid = c.gains_valid = false;
+    c.f_valid = c.gains_valid = c.gains64_valid = false;
 }
 
 void free_all(Ctx &c) {
@@ -83,7 +83,8 @@ void free_all(Ctx &c) {
     dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents); dfree(c.guides);
     c.parents_cap = c.guides_cap = 0; dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
-    dfree(c.fs); dfree(c.fint); dfree(c.freal);
+    dfree(c.fs); dfree(c.fint); dfree(c.freal); dfree(c.Qt); dfree(c.diagt); dfree(c.gains64);
+    c.qt_ld = 0;
     c.real = false;
     c.freal_valid = false;
     c.q_exp = 0;
@@ -349,7 +350,7 @@ int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_lo
     h->rank = rank;
     h->world = world;
     h->k_local = k_local;
-    h->f_valid = h->gains_valid = false;
+    h->f_valid = h->gains_valid = h->gains64_valid = false;
     ubqp::launch_glover(*h, seed_dev, t0, k_local);
     CK_LAUNCH("glover_kernel");
     return UBQP_OK;
@@ -374,7 +375,7 @@ int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int
     h->rank = rank;
     h->world = world;
     h->k_local = k_local;
-    h->f_valid = h->gains_valid = false;
+    h->f_valid = h->gains_valid = h->gains64_valid = false;
     ubqp::launch_glover(*h, seed_dev, t0, k_local, par_dev, n_parents);
     CK_LAUNCH("glover_kernel");
     return UBQP_OK;
@@ -387,7 +388,7 @@ int ubqp_random(ubqp_t h, uint64_t seed, int64_t k_local, int32_t rank, int32_t 
     h->rank = rank;
     h->world = world;
     h->k_local = k_local;
-    h->f_valid = h->gains_valid = false;
+    h->f_valid = h->gains_valid = h->gains64_valid = false;
     ubqp::launch_random(*h, seed, k_local);
     CK_LAUNCH("random_kernel");
     return UBQP_OK;
@@ -406,7 +407,7 @@ int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank
     h->rank = rank;
     h->world = world;
     h->k_local = k_local;
-    h->f_valid = h->gains_valid = false;
+    h->f_valid = h->gains_valid = h->gains64_valid = false;
     ubqp::launch_expand(*h, k_local);
     CK_LAUNCH("expand_kernel");
     return UBQP_OK;
@@ -673,9 +674,13 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
     h->q_ld = ubqp::ascend_capacity(h->n_pad);
     const size_t plane = static_cast<size_t>(h->q_rows) * h->q_ld;
     std::vector<int8_t> L(plane * ubqp::kSlices, 0);
+    h->qt_ld = ubqp::real_qt_ld(h->n_pad);
+    std::vector<int32_t> qt(static_cast<size_t>(h->q_rows) * h->qt_ld, 0), dgt(h->n_pad, 0);
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             long long v = std::llrint(std::ldexp(at(static_cast<int64_t>(i) * n + j), e));
+            qt[static_cast<size_t>(i) * h->qt_ld + j] = static_cast<int32_t>(v);
+            if (i == j) dgt[i] = static_cast<int32_t>(v);
             for (int sl = 0; sl < ubqp::kSlices; ++sl) {
                 const long long r = ((v % 128) + 128) % 128;
                 const long long d = r >= 64 ? r - 128 : r;         // balanced digit in [-64, 63]
@@ -697,12 +702,16 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
               cudaMalloc(&h->surv, k_max * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&h->blk_count, nblk * sizeof(int32_t)) == cudaSuccess;
     for (int sl = 0; ok && sl < ubqp::kSlices; ++sl) ok = cudaMalloc(&h->Qs[sl], plane) == cudaSuccess;
+    ok = ok && cudaMalloc(&h->Qt, qt.size() * sizeof(int32_t)) == cudaSuccess &&
+         cudaMalloc(&h->diagt, dgt.size() * sizeof(int32_t)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_all(*h);
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the real-Q workspace");
     }
-    CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));
+    CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));   // plane gains carry no diagonal (R20)
+    CK(cudaMemcpy(h->Qt, qt.data(), qt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->diagt, dgt.data(), dgt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     for (int sl = 0; sl < ubqp::kSlices; ++sl) {
         CK(cudaMemcpy(h->Qs[sl], L.data() + sl * plane, plane, cudaMemcpyHostToDevice));
         if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
@@ -736,6 +745,7 @@ int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out) {
     ubqp::launch_combine_real(*h, k, h->scratch64 + 8);
     CK_LAUNCH("combine_real_kernel");
     h->freal_valid = true;
+    h->gains64_valid = false;
     bool sync = false;
     if (f_out && k > 0) {
         const bool dev = is_device_ptr(f_out);
@@ -803,3 +813,74 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
 }
 
 }  // extern "C"
+
+int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, double *f_out,
+                     int64_t *fint_out, int32_t *flips_out, uint64_t *bits_out) {
+    GUARD(h);
+    if (!h->real) return fail(h, UBQP_E_STATE, "ubqp: no real-valued Q loaded");
+    if (!h->freal_valid) return fail(h, UBQP_E_STATE, "ubqp: no evaluated real-Q batch");
+    if (m < 0 || m > h->k_local || max_flips < 0 || (!slots && m > 0))
+        return fail(h, UBQP_E_INVALID, "ubqp: bad ascend arguments");
+    const int64_t k = h->k_local;
+    if (!h->gains64_valid && k > 0) {
+        int rc = ensure_gains(h);
+        if (rc) return rc;
+        if (!h->gains64) {
+            if (cudaMalloc(&h->gains64, static_cast<size_t>(h->k_max) * h->n_pad * sizeof(int64_t)) != cudaSuccess) {
+                cudaGetLastError();
+                h->gains64 = nullptr;
+                return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the int64 gains buffer");
+            }
+        }
+        // Delta~ = Qt_jj + sum_s 128^s 2 (1 - 2x) Y_s: plane gains (zero diagonal) combined exactly
+        for (int sl = 0; sl < ubqp::kSlices; ++sl) {
+            ubqp::launch_eval_tc(*h, k, true, sl, h->fs + sl * h->k_max);
+            CK_LAUNCH("eval_tc_kernel (plane gains)");
+            ubqp::launch_gains_combine(*h, k, sl);
+            CK_LAUNCH("gains_combine_kernel");
+        }
+        h->gains64_valid = true;
+    }
+    int rc = ensure_asc(h, m > 0 ? m : 1);
+    if (rc) return rc;
+    const int32_t *slots_dev = slots;
+    if (m > 0 && !is_device_ptr(slots)) {
+        for (int64_t i = 0; i < m; ++i)
+            if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        slots_dev = h->asc_slots;
+    }
+    if (m == 0) return UBQP_OK;
+    // device outputs pass through; host outputs go through scratch (f as int64 bits in asc_f)
+    const bool f_dev = f_out && is_device_ptr(f_out);
+    const bool i_dev = fint_out && is_device_ptr(fint_out);
+    const bool fl_dev = flips_out && is_device_ptr(flips_out);
+    const bool b_dev = bits_out && is_device_ptr(bits_out);
+    double *fr_d = f_dev ? f_out : (f_out ? reinterpret_cast<double *>(h->asc_f) : nullptr);
+    int64_t *fi_d = i_dev ? fint_out : nullptr;
+    int64_t *fi_host_tmp = nullptr;
+    if (fint_out && !i_dev) {
+        // second scratch: reuse the per-slot stats area of the planes (fs has kSlices * k_max)
+        fi_d = h->fs;
+        fi_host_tmp = fint_out;
+    }
+    int32_t *fl_d = fl_dev ? flips_out : h->asc_flips;
+    uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
+    if (ubqp::launch_ascend_real(*h, slots_dev, m, max_flips, fr_d, fi_d, fl_d, b_d))
+        return fail(h, UBQP_E_RANGE, "ubqp: n outside the real ascent kernel range");
+    CK_LAUNCH("ascend_real_kernel");
+    bool sync = false;
+    if (f_out && !f_dev) { CK(cudaMemcpyAsync(f_out, fr_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (fi_host_tmp) { CK(cudaMemcpyAsync(fi_host_tmp, fi_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (flips_out && !fl_dev) { CK(cudaMemcpyAsync(flips_out, fl_d, m * 4, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
+    if (bits_out && !b_dev) {
+        CK(cudaMemcpyAsync(bits_out, b_d, m * h->W64 * 8, cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
+    }
+    if (sync) CK(cudaStreamSynchronize(h->stream));
+    if (!fl_dev && flips_out) {
+        for (int64_t i = 0; i < m; ++i)
+            if (flips_out[i] < 0) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
+    }
+    return UBQP_OK;
+}

@@ -73,6 +73,13 @@ struct Ctx {
     int64_t *fs = nullptr;       // [kSlices][k_max] per-plane x^t L_s x
     int64_t *fint = nullptr;     // [k_max] integer image f~ = sum_s 128^s f_s
     double *freal = nullptr;     // [k_max] f = 2^-q_exp f~
+    // real-Q ascent (R20): the image Qt = rint(Q 2^e) as int32 rows [q_rows][qt_ld] (zero
+    // padded), its diagonal, and int64 gains of the batch
+    int32_t *Qt = nullptr;
+    int qt_ld = 0;
+    int32_t *diagt = nullptr;    // [n_pad]
+    int64_t *gains64 = nullptr;  // [k_max][n_pad]
+    bool gains64_valid = false;
     bool freal_valid = false;
     int64_t launches = 0;
 };
@@ -94,6 +101,11 @@ void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
 // screen.cu
 void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);
 void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
+// ascend_real.cu (R20)
+int real_qt_ld(int n_pad);
+void launch_gains_combine(Ctx &c, int64_t k, int plane);   // gains64 (+)= gains << 7 plane
+int launch_ascend_real(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, double *f_dev,
+                       int64_t *fint_dev, int32_t *flips_dev, uint64_t *bits_dev);
 // ascend.cu
 int ascend_capacity(int n_pad);   // variables covered by the default ascent shape (>= n_pad)
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,

@@ -25,7 +25,7 @@ Q_N, Q_NPAD, Q_W64, Q_KMAX, Q_KLOCAL, Q_LAUNCHES, Q_STREAM = range(7)
 EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ubqp_load_Q",
            "ubqp_diversify", "ubqp_blend", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
            "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_relink", "ubqp_sync", "ubqp_query",
-           "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real"]
+           "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real", "ubqp_ascend_real"]
 UBQP_F32, UBQP_F64 = 1, 2
 Q_REAL_EXP, Q_IS_REAL = 7, 8
 
@@ -84,6 +84,7 @@ def load_library(path: Path | str | None = None):
         "ubqp_load_Q_real": ([P, i32, ctypes.c_int, P, i64], ctypes.c_int),
         "ubqp_eval_batch_real": ([P, P, P], ctypes.c_int),
         "ubqp_screen_real": ([P, dbl, dbl, dbl, P, P, P], ctypes.c_int),
+        "ubqp_ascend_real": ([P, P, i64, i32, P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -221,6 +222,10 @@ class Ubqp:
         self._ck(self.lib.ubqp_screen_real(self.h, float(lam), float(mean), float(max_value), _ptr(surv_out),
                                            ctypes.byref(m), ctypes.byref(T)))
         return m.value, T.value
+
+    def ascend_real(self, slots, m: int, max_flips: int, f_out=None, fint_out=None, flips_out=None, bits_out=None):
+        self._ck(self.lib.ubqp_ascend_real(self.h, _ptr(slots), m, max_flips, _ptr(f_out), _ptr(fint_out),
+                                           _ptr(flips_out), _ptr(bits_out)))
 
     def sync(self):
         self._ck(self.lib.ubqp_sync(self.h))

@@ -112,3 +112,74 @@ def test_real_full_size_sampled(n):
     idx = np.array([0, 1, 777, K - 1])
     X = oracle.random_solutions(n, 4, K)[idx]
     _check(Q, X, f[idx], u.real_exp)
+
+
+@pytest.mark.parametrize("n", [1, 2, 65, 300, 1100, 2500])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ascend_real_matches_oracle(n, dtype):
+    """R20: the real-Q walk on the fixed-point image is bit-exact against the oracle's walk
+    on its own image (x, flips, f~), f = 2^-e f~ exactly, and f is within R3 of fsum."""
+    Q = generate_Q_real(n, 0.7, seed=100 + n, dtype=dtype)
+    K = 24 if n >= 1100 else 96
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    u.random(n + 5, K)
+    u.eval_batch_real()
+    X0 = oracle.random_solutions(n, n + 5, K)
+    slots = np.arange(K, dtype=np.int32)[::-1].copy()
+    f = np.zeros(K, np.float64)
+    fi = np.zeros(K, np.int64)
+    fl = np.zeros(K, np.int32)
+    b = np.zeros((K, u.W64), np.uint64)
+    u.ascend_real(slots, K, 10 * n, f, fi, fl, b)
+    Xa, fa, ff, ofl, e = oracle.ascend_real(Q.astype(np.float64), X0[slots], 10 * n, nthreads=8)
+    assert e == u.real_exp
+    assert np.array_equal(unpack_bits(b, n), Xa) and np.array_equal(fl, ofl) and np.array_equal(fi, fa)
+    assert np.array_equal(f, ff)
+    _check(Q, Xa, f, e)
+
+
+def test_ascend_real_integer_Q_equals_integer_ascent_and_device_outputs():
+    n, K = 700, 200
+    Q = generate_Q(n, 0.5, seed=13)
+    Q[0, 0] = 100
+    ui = Ubqp(0)
+    ui.load_Q(Q, K)
+    ui.random(4, K)
+    ui.eval_batch(1)
+    fo = np.zeros(K, np.int64)
+    flo = np.zeros(K, np.int32)
+    bo = np.zeros((K, ui.W64), np.uint64)
+    ui.ascend(np.arange(K, dtype=np.int32), K, 10 * n, fo, flo, bo)
+    ur = Ubqp(0)
+    ur.load_Q_real(Q.astype(np.float64), K)
+    ur.random(4, K)
+    ur.eval_batch_real()
+    assert ur.real_exp == 20
+    sl = torch.arange(K, dtype=torch.int32, device="cuda")
+    f = torch.zeros(K, dtype=torch.float64, device="cuda")
+    fi = torch.zeros(K, dtype=torch.int64, device="cuda")
+    fl = torch.zeros(K, dtype=torch.int32, device="cuda")
+    b = torch.zeros((K, ur.W64), dtype=torch.int64, device="cuda")
+    ur.ascend_real(sl, K, 10 * n, f, fi, fl, b)
+    torch.cuda.synchronize()
+    assert np.array_equal(fl.cpu().numpy(), flo) and np.array_equal(b.cpu().numpy().view(np.uint64), bo)
+    assert np.array_equal(fi.cpu().numpy(), fo * 2**20) and np.array_equal(f.cpu().numpy(), fo.astype(np.float64))
+
+
+def test_ascend_real_errors():
+    u = Ubqp(0)
+    Q = generate_Q(50, 0.5, seed=1)
+    u.load_Q(Q, 8)
+    u.random(1, 8)
+    u.eval_batch(0)
+    with pytest.raises(UbqpError):                  # integer Q loaded
+        u.ascend_real(np.arange(8, dtype=np.int32), 8, 100)
+    ur = Ubqp(0)
+    ur.load_Q_real(Q.astype(np.float64), 8)
+    ur.random(1, 8)
+    with pytest.raises(UbqpError):                  # not evaluated yet
+        ur.ascend_real(np.arange(8, dtype=np.int32), 8, 100)
+    ur.eval_batch_real()
+    with pytest.raises(UbqpError):
+        ur.ascend_real(np.array([0, 8], np.int32), 2, 100)
