@@ -355,6 +355,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["table1_eval_1000"] = table1_eval(local_rank)
         out["config1_round"] = config1_round(local_rank)
         out["real_q_eval"] = real_q_eval(local_rank)
+        out["real_q_ascent"] = real_q_ascent(local_rank)
         out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
         out["ascent_microbench"] = ascent_microbench(local_rank)
         out["relink_microbench"] = relink_microbench(local_rank)
@@ -554,6 +555,37 @@ def relink_microbench(device):
     u.close()
     return {"n": n, "m": m, "ms": ms, "steps": steps, "steps_per_s": steps / (ms * 1e-3),
             "TB_per_s_qrow": steps * n / (ms * 1e-3) / 1e12}
+
+
+def real_q_ascent(device):
+    """R20: real-valued Q (n = 7000 dense, U(-100,100) float32), 8192 random starts ascended
+    exactly on the fixed-point image (int64 gains, Qt rows int32 = 4 qt_ld bytes per step,
+    HBM-resident): flip steps/s and Qt-row GB/s."""
+    import torch
+
+    from inputs import generate_Q_real
+    from paper_1706_00037_b200 import Ubqp
+    n, m = 7000, 8192
+    Q = generate_Q_real(n, 1.0, seed=4, dtype=np.float32)
+    u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+    u.load_Q_real(Q, m)
+    u.random(5, m)
+    u.eval_batch_real()
+    slots = torch.arange(m, dtype=torch.int32, device="cuda")
+    fl = torch.zeros(m, dtype=torch.int32, device="cuda")
+    u.ascend_real(slots, m, 10 * n, None, None, fl)          # forms the int64 gains
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    u.ascend_real(slots, m, 10 * n, None, None, fl)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    steps = int(fl.sum().item())
+    row_bytes = 4 * n                                         # algorithmic: one int32 Qt row per step
+    u.close()
+    return {"n": n, "m": m, "ms": ms, "steps": steps, "steps_per_s": steps / (ms * 1e-3),
+            "GB_per_s_qt_rows": steps * row_bytes / (ms * 1e-3) / 1e9,
+            "note": "Qt (int32, 196 MB) exceeds L2: HBM-bound, vs the measured copy bandwidth"}
 
 
 def real_q_eval(device):
