@@ -56,25 +56,27 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         }
         return;
     }
-    long long G[NPT];
+    // gains in shared memory, [q][t] (conflict-free 8-byte words): 3 solutions per SM at
+    // n = 7000 instead of 2 with register gains (the step waits on an HBM row fetch, so
+    // solutions in flight set the rate)
+    extern __shared__ long long s_G[];
     uint64_t xm = 0;
     const int64_t *grow = g64 + s * n_pad;
     const uint64_t *xrow = Xb + s * W64;
+    long long bv = LLONG_MIN;
+    int bq = 0;
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
         const int j = t + kRB * q;
-        G[q] = j < n ? grow[j] : kRPad;
+        const long long g = j < n ? grow[j] : kRPad;
+        s_G[q * kRB + t] = g;
+        if (g > bv) { bv = g; bq = q; }
         if (j < n) xm |= ((xrow[j >> 6] >> (j & 63)) & 1ull) << q;
     }
     long long fv = fint_in[s];
     int flips = 0;
     for (;;) {
-        // ---- argmax: thread -> warp (largest gain, then lowest j) -> block
-        long long bv = G[0];
-        int bq = 0;
-#pragma unroll
-        for (int q = 1; q < NPT; ++q)
-            if (G[q] > bv) { bv = G[q]; bq = q; }
+        // ---- argmax: thread (tracked by the last update) -> warp (largest gain, then lowest j) -> block
         unsigned bj = (static_cast<unsigned>(t + kRB * bq) << 1) | static_cast<unsigned>((xm >> bq) & 1ull);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -98,7 +100,7 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         }
         if (gv <= 0 || flips == max_flips) break;
 
-        // ---- flip k*
+        // ---- flip k*: update every gain and track the next thread maximum
         const int kstar = static_cast<int>(gj >> 1);
         const long long d2 = (gj & 1u) ? -2 : 2;          // 2 d, d = 1 - 2 x_k*
         fv += gv;
@@ -108,12 +110,23 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         int32_t qv[NPT];
 #pragma unroll
         for (int q = 0; q < NPT; ++q) qv[q] = __ldg(row + kRB * q);   // rows padded to qt_ld
+        // the owner parks Delta_k* out of reach of the max for the uniform pass, then stores -gv
+        if (own >= 0) s_G[own * kRB + t] = kRPad;
+        const int c2 = static_cast<int>(d2);
+        bv = LLONG_MIN;
+        bq = 0;
 #pragma unroll
         for (int q = 0; q < NPT; ++q) {
-            const long long inc = ((xm >> q) & 1ull) ? -d2 * qv[q] : d2 * qv[q];
-            G[q] = q == own ? -gv : G[q] + inc;
+            const int coef = ((xm >> q) & 1ull) ? -c2 : c2;           // 2 d (1 - 2 x_j)
+            const long long g = s_G[q * kRB + t] + static_cast<long long>(coef) * qv[q];   // IMAD.WIDE
+            s_G[q * kRB + t] = g;
+            if (g > bv) { bv = g; bq = q; }
         }
-        if (own >= 0) xm ^= 1ull << own;
+        if (own >= 0) {
+            s_G[own * kRB + t] = -gv;
+            if (-gv > bv || (-gv == bv && own < bq)) { bv = -gv; bq = own; }
+            xm ^= 1ull << own;
+        }
     }
 
     // ---- outputs
@@ -141,9 +154,16 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
 template <int NPT>
 void launch_real_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, double *f_dev, int64_t *fint_dev,
                       int32_t *flips_dev, uint64_t *bits_dev) {
-    constexpr int kRegs = 3 * NPT + 40;
-    constexpr int kMinB = 65536 / (kRB * kRegs) < 1 ? 1 : 65536 / (kRB * kRegs);
-    ascend_real_kernel<NPT, kMinB><<<static_cast<unsigned>(m), kRB, 0, c.stream>>>(
+    constexpr int kSmem = NPT * kRB * 8;
+    constexpr int kByS = (228 * 1024) / (kSmem + 3 * 1024);
+    constexpr int kByR = 65536 / (kRB * (NPT + 40));
+    constexpr int kMinB = (kByS < kByR ? kByS : kByR) < 1 ? 1 : (kByS < kByR ? kByS : kByR);
+    static bool attr = false;                 // one opt-in per instantiation (> 48 KB dynamic)
+    if (!attr) {
+        cudaFuncSetAttribute(ascend_real_kernel<NPT, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        attr = true;
+    }
+    ascend_real_kernel<NPT, kMinB><<<static_cast<unsigned>(m), kRB, kSmem, c.stream>>>(
         slots, max_flips, c.n, c.n_pad, c.qt_ld, c.W64, c.k_local, c.Qt, c.gains64, c.fint, c.Xb, c.q_exp, f_dev,
         fint_dev, flips_dev, bits_dev);
 }
