@@ -1,3 +1,4 @@
+"""bench.real_q_ascent on its own (R20 real-Q ascent measurement; UBQP_LIB for A/B)."""
 import json
 import sys
 from pathlib import Path
