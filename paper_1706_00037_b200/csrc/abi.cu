@@ -683,7 +683,9 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
             if (i == j) dgt[i] = static_cast<int32_t>(v);
             for (int sl = 0; sl < ubqp::kSlices; ++sl) {
                 const long long r = ((v % 128) + 128) % 128;
-                const long long d = r >= 64 ? r - 128 : r;         // balanced digit in [-64, 63]
+                // balanced digits in [-64, 63]; the top digit takes the remainder, which is
+                // round(v / 2^21) in [-64, 64] for |v| <= 2^27 - 1 (64 fits int8)
+                const long long d = sl == ubqp::kSlices - 1 ? v : (r >= 64 ? r - 128 : r);
                 L[sl * plane + static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(d);
                 v = (v - d) / 128;
             }

@@ -61,3 +61,57 @@ def test_round_matches_oracle(n, K, density, qmax, seed, lam, max_flips, glover)
         assert np.array_equal(unpack_bits(ba, n), Xr)
         assert key[0] == max(oracle.max_key(int(fr[i]), int(s[i])) for i in range(m))
     u.close()
+
+
+@settings(max_examples=60, deadline=None)
+@given(n=st.integers(1, 600), K=st.integers(1, 300), P=st.integers(1, 9), qmax=st.sampled_from([1, 50, 127]),
+       seed=st.integers(0, 2**31 - 1), t0=st.integers(0, 10**6))
+def test_blend_and_relink_match_oracle(n, K, P, qmax, seed, t0):
+    """O4b blend bits and O11 relinking outputs on arbitrary shapes (R11b, R19)."""
+    Q = generate_Q(n, 0.5, -qmax, qmax, seed=seed)
+    rng = np.random.default_rng(seed)
+    s0 = rng.integers(0, 2, size=n).astype(np.uint8)
+    par = rng.integers(0, 2, size=(P, n)).astype(np.uint8)
+    u = Ubqp(0)
+    u.load_Q(Q, K)
+    u.blend(pack_bits(s0)[0], pack_bits(par), P, t0, K)
+    B = np.zeros((K, u.W64), np.uint64)
+    u.get_batch(B)
+    X = oracle.blend(s0, par, t0, K)
+    assert np.array_equal(unpack_bits(B, n), X)
+    f0 = np.zeros(K, np.int64)
+    u.eval_batch(UBQP_EMIT_GAINS, f0)
+    f = np.zeros(K, np.int64)
+    stp = np.zeros(K, np.int32)
+    ln = np.zeros(K, np.int32)
+    b = np.zeros((K, u.W64), np.uint64)
+    u.relink(pack_bits(par), P, np.arange(K, dtype=np.int32), K, f, stp, ln, b)
+    ob, of, os_, ol = oracle.relink(Q, X, f0, par, nthreads=8)
+    assert np.array_equal(ln, ol) and np.array_equal(stp, os_) and np.array_equal(f, of)
+    assert np.array_equal(unpack_bits(b, n), ob)
+    u.close()
+
+
+@settings(max_examples=40, deadline=None)
+@given(n=st.integers(1, 500), K=st.integers(1, 120), scale=st.sampled_from([1e-3, 1.0, 37.5, 1e6]),
+       seed=st.integers(0, 2**31 - 1), f32=st.booleans(), max_flips=st.sampled_from([0, 3, 10**6]))
+def test_real_ascent_matches_oracle(n, K, scale, seed, f32, max_flips):
+    """R20 real-Q ascent on arbitrary shapes and coefficient scales."""
+    rng = np.random.default_rng(seed)
+    A = rng.uniform(-scale, scale, size=(n, n))
+    Q = np.triu(A) + np.triu(A, 1).T
+    if f32:
+        Q = Q.astype(np.float32)
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    u.random(seed, K)
+    u.eval_batch_real()
+    fi = np.zeros(K, np.int64)
+    fl = np.zeros(K, np.int32)
+    b = np.zeros((K, u.W64), np.uint64)
+    u.ascend_real(np.arange(K, dtype=np.int32), K, max_flips, None, fi, fl, b)
+    Xa, fa, ff, ofl, e = oracle.ascend_real(Q.astype(np.float64), oracle.random_solutions(n, seed, K), max_flips,
+                                            nthreads=8)
+    assert e == u.real_exp
+    assert np.array_equal(fi, fa) and np.array_equal(fl, ofl) and np.array_equal(unpack_bits(b, n), Xa)
+    u.close()

@@ -183,3 +183,24 @@ def test_ascend_real_errors():
     ur.eval_batch_real()
     with pytest.raises(UbqpError):
         ur.ascend_real(np.array([0, 8], np.int32), 2, 100)
+
+
+def test_real_top_limb_at_64():
+    """Regression: max|Q| just below a power of two puts |rint(Q 2^e)| above the balanced
+    4-digit range (63 * (1 + 128 + 128^2 + 128^3)); the top limb must then hold 64."""
+    Q = np.array([[0.999, -0.5, 0.25], [-0.5, -0.9999, 0.125], [0.25, 0.125, 0.75]])
+    K = 8
+    u = Ubqp(0)
+    u.load_Q_real(Q, K)
+    assert u.real_exp == 27
+    X = np.array([[1, 1, 1], [1, 0, 0], [0, 1, 0], [1, 0, 1], [0, 1, 1], [1, 1, 0], [0, 0, 1], [0, 0, 0]], np.uint8)
+    u.set_batch(pack_bits(X), K)
+    f = np.zeros(K, np.float64)
+    u.eval_batch_real(f)
+    Qt, e = oracle.real_image(Q)
+    ft = oracle.eval_batch(Qt.astype(np.int32), X)
+    assert np.array_equal(f, np.ldexp(ft.astype(np.float64), -e))
+    fi = np.zeros(K, np.int64)
+    u.ascend_real(np.arange(K, dtype=np.int32), K, 100, None, fi)
+    Xa, fa, _, _, _ = oracle.ascend_real(Q, X, 100)
+    assert np.array_equal(fi, fa)
