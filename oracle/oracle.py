@@ -22,7 +22,7 @@ __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
     "first_derivative_start", "relink", "polish", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
-    "real_image", "ascend_real",
+    "real_image", "ascend_real", "run_rounds_real",
 ]
 
 
@@ -378,3 +378,47 @@ def ascend_real(Q, X, max_flips: int, nthreads: int = 1):
     f0 = eval_batch(Qt.astype(np.int32), X, nthreads)
     Xa, fa, fl = ascend(Qt.astype(np.int32), X, f0, max_flips, nthreads)
     return Xa, fa, np.ldexp(fa.astype(np.float64), -e), fl, e
+
+
+# O8 on a real Q (R20): the batched rounds of run_rounds with every decision taken on the
+# fixed-point image Qt (sampling mean, first-derivative start, f~, T in binary64 on f = 2^-e f~)
+def run_rounds_real(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
+                    world: int = 1, nthreads: int = 1):
+    """Returns (best f~ int, best x, trajectory [(round, f~)], e).  Mean = 2^-e (sum f~ / K)
+    (one correctly rounded division), Max = 2^-e max(incumbent, batch max),
+    T = Mean + lam (Max - Mean) in binary64, survivors f > T, incumbent replaced iff the
+    best ascended f~ is strictly greater (ties: lowest g)."""
+    import math
+    Qt, e = real_image(Q)
+    Qi = Qt.astype(np.int32)
+    n = Qi.shape[0]
+    mean_sum = 0
+    for r in range(world):
+        mean_sum += int(eval_batch(Qi, random_solutions(n, sample_seed, len(range(r, K, world)), r, world),
+                                   nthreads).sum())
+    mean = math.ldexp(mean_sum / K, -e)
+    inc_x = first_derivative_start(Qi)
+    inc_f = xQx(Qi, inc_x)
+    traj = [(0, inc_f)]
+    for rnd in range(1, rounds + 1):
+        t0 = (rnd - 1) * K
+        Xs = [diversify(inc_x, t0, len(range(r, K, world)), r, world) for r in range(world)]
+        fs = [eval_batch(Qi, Xr, nthreads) for Xr in Xs]
+        bmax = max(int(fr.max()) for fr in fs if fr.size)
+        maxv = math.ldexp(float(max(inc_f, bmax)), -e)
+        T = mean + lam * (maxv - mean)
+        best = None
+        for r in range(world):
+            fr = np.ldexp(fs[r].astype(np.float64), -e)
+            s = np.flatnonzero(fr > T)
+            if s.size == 0:
+                continue
+            Xa, fa, _ = ascend(Qi, Xs[r][s], fs[r][s], max_flips, nthreads)
+            for i, slot in enumerate(s):
+                cand = (int(fa[i]), -(r + int(slot) * world))
+                if best is None or cand > best[0]:
+                    best = (cand, Xa[i].copy())
+        if best is not None and best[0][0] > inc_f:
+            inc_f, inc_x = best[0][0], best[1]
+            traj.append((rnd, inc_f))
+    return inc_f, inc_x, traj, e

@@ -600,3 +600,22 @@ def test_real_ascent_value_within_rounding_bound():
     for x, f in zip(Xa, ff):
         S = int(x.sum())
         assert abs(f - oracle.xQx_real(Q, x)) <= S * S * 2.0 ** (-(e + 1)) + 1e-9
+
+
+def test_real_rounds_integer_Q_reduce_to_integer_rounds_and_world_invariance():
+    # integer-valued real Q (max |Q| = 100): the image is 2^20 Q, so every decision equals
+    # the integer round loop's and f~ = 2^20 f (same trajectory rounds)
+    Q = generate_Q(60, 0.5, -100, 100, seed=71).astype(np.int32)
+    Q[0, 0] = 100
+    a = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3)
+    b = oracle.run_rounds_real(Q.astype(np.float64), K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3)
+    assert b[3] == 20 and b[0] == a[0] * 2**20 and np.array_equal(b[1], a[1])
+    assert [(r, v) for r, v in b[2]] == [(r, v * 2**20) for r, v in a[2]]
+    rng = np.random.default_rng(72)
+    A = rng.uniform(-10, 10, size=(45, 45))
+    Qr = np.triu(A) + np.triu(A, 1).T
+    c = oracle.run_rounds_real(Qr, K=40, rounds=3, lam=0.3, max_flips=500, sample_seed=4)
+    d = oracle.run_rounds_real(Qr, K=40, rounds=3, lam=0.3, max_flips=500, sample_seed=4, world=3)
+    assert c[0] == d[0] and np.array_equal(c[1], d[1]) and c[2] == d[2]
+    Qt, e = oracle.real_image(Qr)
+    assert c[0] == oracle.xQx(Qt.astype(np.int32), c[1])
