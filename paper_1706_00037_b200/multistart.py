@@ -256,3 +256,115 @@ class MultiStart:
                 inc_f, inc_bits = res
                 traj.append((rounds + 1, inc_f))
         return inc_f, inc_bits, traj
+
+
+# ---------------------------------------------------------------- real-valued Q (R20)
+def combine_real_stats(st, group=None):
+    """ubqp_stats_real of each rank -> (sum f~ as a Python int, count, max f~): one all_gather
+    of four int64 words per rank, combined exactly on the host (the sum is int128)."""
+    _, world = dist_info(group)
+    words = torch.tensor([st.sum_hi, st.sum_lo, st.count, st.max_fint], dtype=torch.int64)
+    if world > 1:
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        words = words.to(dev)
+        out = [torch.zeros_like(words) for _ in range(world)]
+        dist.all_gather(out, words, group=group)
+        rows = [o.cpu().tolist() for o in out]
+    else:
+        rows = [words.tolist()]
+    total = sum((hi << 64) | (lo & (2**64 - 1)) for hi, lo, _, _ in rows)
+    return total, sum(r[2] for r in rows), max(r[3] for r in rows if r[2] > 0)
+
+
+class MultiStartReal:
+    """Figure 2 rounds on a real-valued Q (R20): decisions on the fixed-point image, f~ exact,
+    reported f = 2^-e f~.  Same sharding and exchange pattern as MultiStart."""
+
+    def __init__(self, Q: np.ndarray, K: int, lam: float = 0.5, max_flips: int | None = None,
+                 device: int | None = None, group=None):
+        from .ubqp import ubqp_stats_real
+        self.rank, self.world = dist_info(group)
+        self.group = group
+        self.device = torch.cuda.current_device() if device is None else device
+        self.n = int(Q.shape[0])
+        self.K = int(K)
+        self.k_local = len(range(self.rank, self.K, self.world))
+        self.lam = float(lam)
+        self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
+        self.stream = torch.cuda.Stream(device=self.device)
+        torch.cuda.set_stream(self.stream)
+        self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
+        self.u.load_Q_real(np.ascontiguousarray(Q), max(self.k_local, 1))
+        self.e = self.u.real_exp
+        self.W64 = self.u.W64
+        dv = torch.device("cuda", self.device)
+        kl = max(self.k_local, 1)
+        self.st = ubqp_stats_real()
+        self.surv = torch.zeros(kl, dtype=torch.int32, device=dv)
+        self.fint = torch.zeros(kl, dtype=torch.int64, device=dv)
+        self.flips = torch.zeros(kl, dtype=torch.int32, device=dv)
+        self.bits = torch.zeros((kl, self.W64), dtype=torch.int64, device=dv)
+        self.fd_bits = torch.zeros(self.W64, dtype=torch.int64, device=dv)
+
+    def sample_mean(self, seed: int):
+        self.u.random(seed, self.k_local, self.rank, self.world)
+        self.u.eval_batch_real(None, self.st)
+        total, count, _ = combine_real_stats(self.st, self.group)
+        return total, count
+
+    def first_derivative(self):
+        self.u.first_derivative(self.fd_bits)
+        self.u.set_batch(self.fd_bits, 1, 0, 1)
+        self.u.eval_batch_real(None, self.st)
+        return self.fd_bits.clone(), int(self.st.max_fint)
+
+    def round(self, seed_bits, t0: int, inc_fint: int, mean_pair):
+        """-> (m on this rank, T, best f~ over all ranks or None, its bits)."""
+        import math
+        u = self.u
+        u.diversify(seed_bits, t0, self.k_local, self.rank, self.world)
+        u.eval_batch_real(None, self.st)
+        _, _, bmax = combine_real_stats(self.st, self.group)
+        mean = math.ldexp(mean_pair[0] / mean_pair[1], -self.e)
+        maxv = math.ldexp(float(max(inc_fint, bmax)), -self.e)
+        m, T = u.screen_real(self.lam, mean, maxv, self.surv)
+        best = None
+        if m > 0:
+            u.ascend_real(self.surv, m, self.max_flips, None, self.fint, self.flips, self.bits)
+            fi = self.fint[:m]
+            mx = int(fi.max().item())
+            i = int(torch.nonzero(fi == mx)[0].item())      # lowest slot = lowest g among ties
+            best = (mx, self.rank + int(self.surv[i].item()) * self.world, i)
+        # global best: highest f~, then lowest g; the owner broadcasts the bits
+        cand = torch.tensor([best[0], best[1]] if best else [-(2**62), 2**62], dtype=torch.int64)
+        if self.world > 1:
+            dev = self.bits.device if dist.get_backend(self.group) == "nccl" else "cpu"
+            cand = cand.to(dev)
+            out = [torch.zeros_like(cand) for _ in range(self.world)]
+            dist.all_gather(out, cand, group=self.group)
+            rows = [o.cpu().tolist() for o in out]
+        else:
+            rows = [cand.tolist()]
+        gf, gg = max(rows, key=lambda r: (r[0], -r[1]))
+        if gf == -(2**62):
+            return m, T, None, None
+        owner = gg % self.world
+        row = self.bits[best[2]].clone() if (best and owner == self.rank) else torch.zeros_like(self.bits[0])
+        if self.world > 1:
+            src = dist.get_global_rank(self.group, owner) if self.group is not None else owner
+            if dist.get_backend(self.group) != "nccl":
+                row = row.cpu()
+            dist.broadcast(row, src=src, group=self.group)
+            row = row.to(self.bits.device)
+        return m, T, gf, row
+
+    def run(self, rounds: int, sample_seed: int, t_start: int = 0):
+        mean = self.sample_mean(sample_seed)
+        inc_bits, inc_f = self.first_derivative()
+        traj = [(0, inc_f)]
+        for r in range(1, rounds + 1):
+            _, _, bf, bb = self.round(inc_bits, t_start + (r - 1) * self.K, inc_f, mean)
+            if bf is not None and bf > inc_f:
+                inc_f, inc_bits = bf, bb.clone()
+                traj.append((r, inc_f))
+        return inc_f, inc_bits, traj

@@ -204,3 +204,18 @@ def test_real_top_limb_at_64():
     u.ascend_real(np.arange(K, dtype=np.int32), K, 100, None, fi)
     Xa, fa, _, _, _ = oracle.ascend_real(Q, X, 100)
     assert np.array_equal(fi, fa)
+
+
+@pytest.mark.parametrize("n,K,rounds,lam", [(60, 400, 3, 0.4), (500, 2000, 3, 0.3)])
+def test_multistart_real_matches_oracle(n, K, rounds, lam):
+    """Figure-2 rounds on a real Q (R20) against oracle.run_rounds_real: trajectory of exact
+    f~ values and the final solution."""
+    from paper_1706_00037_b200.multistart import MultiStartReal
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-50, 50, size=(n, n))
+    Q = np.triu(A) + np.triu(A, 1).T
+    ms = MultiStartReal(Q, K, lam=lam, max_flips=10 * n)
+    best, bits, traj = ms.run(rounds, sample_seed=5)
+    ob, ox, otraj, e = oracle.run_rounds_real(Q, K, rounds, lam, 10 * n, sample_seed=5, nthreads=8)
+    assert ms.e == e and best == ob and traj == otraj
+    assert np.array_equal(unpack_bits(bits.cpu().numpy().view(np.uint64)[None, :], n)[0], ox)

@@ -109,3 +109,40 @@ def test_blend_pool_update_matches_oracle_rules():
         assert len(pool_o) == len(pool_t)
         for a, b in zip(pool_o, pool_t):
             assert np.array_equal(pack_bits(a)[0].view(np.int64), b.numpy())
+
+
+def _worker_real(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1706_00037_b200.multistart import combine_real_stats
+
+        class St:                                   # the ubqp_stats_real fields of one rank
+            pass
+        rng = np.random.default_rng(100 + rank)
+        v = [int(x) for x in rng.integers(-(2**60), 2**60, size=5)] if rank != 1 else []
+        total = sum(v)
+        st = St()
+        st.sum_hi, st.sum_lo = total >> 64, total & (2**64 - 1)
+        if st.sum_lo >= 2**63:
+            st.sum_lo -= 2**64                      # the C struct stores a signed int64 word
+        st.count = len(v)
+        st.max_fint = max(v) if v else -(2**63)
+        out[rank] = combine_real_stats(st)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_real_stats_exchange_is_exact(world):
+    """MultiStartReal's exchange: int128 sums of f~ across ranks (one rank empty) are exact."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_real, args=(world, _free_port(), out), nprocs=world, join=True)
+    vals = []
+    for r in range(world):
+        if r != 1:
+            vals += [int(x) for x in np.random.default_rng(100 + r).integers(-(2**60), 2**60, size=5)]
+    for r in range(world):
+        assert out[r] == (sum(vals), len(vals), max(vals))
