@@ -81,12 +81,25 @@ __device__ __forceinline__ void owner_fix(int (&K)[NCH][16], uint32_t (&m)[NCH][
     }
 }
 
-#define UBQP_CASE(L) \
-    case L:          \
-        owner_fix<L, NCH>(K, m, w, gv, x_new, kfix); \
+template <int C, int NCH>
+__device__ __forceinline__ void owner_fix_chunk(int (&K)[NCH][16], uint32_t (&m)[NCH][4],
+                                                const uint4 (&w)[NCH], int e, int gv, int x_new, int off) {
+#define UBQP_ECASE(E) \
+    case E:           \
+        owner_fix<C * 16 + E, NCH>(K, m, w, gv, x_new, off); \
         break;
-#define UBQP_CASE8(B) UBQP_CASE(B) UBQP_CASE(B + 1) UBQP_CASE(B + 2) UBQP_CASE(B + 3) \
-                      UBQP_CASE(B + 4) UBQP_CASE(B + 5) UBQP_CASE(B + 6) UBQP_CASE(B + 7)
+    switch (e) {
+        UBQP_ECASE(0) UBQP_ECASE(1) UBQP_ECASE(2) UBQP_ECASE(3) UBQP_ECASE(4) UBQP_ECASE(5)
+        UBQP_ECASE(6) UBQP_ECASE(7) UBQP_ECASE(8) UBQP_ECASE(9) UBQP_ECASE(10) UBQP_ECASE(11)
+        UBQP_ECASE(12) UBQP_ECASE(13) UBQP_ECASE(14) UBQP_ECASE(15)
+        default: break;
+    }
+#undef UBQP_ECASE
+}
+#define UBQP_CCASE(C) \
+    case C:           \
+        if constexpr (C < NCH) owner_fix_chunk<C, NCH>(K, m, w, kstar & 15, gv, x_new, kfix); \
+        break;
 
 // Path relinking (O11, NEXT-4; R19) reuses the ascent loop: variables outside
 // D = {j : x_j != y_j} carry keys lowered by kOff = 2^30, below every key in D while
@@ -252,13 +265,10 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
                 w[c] = cvalid[c] ? __ldg(qrow + c * (A::CHUNK / 16)) : make_uint4(0, 0, 0, 0);
         }
         if (((kstar % A::CHUNK) >> 4) == t) {
-            const int li = (kstar / A::CHUNK) * 16 + (kstar & 15);
             const int x_new = xk ^ 1;
-            switch (li) {
-                UBQP_CASE8(0) UBQP_CASE8(8) UBQP_CASE8(16) UBQP_CASE8(24)
-                UBQP_CASE8(32) UBQP_CASE8(40) UBQP_CASE8(48) UBQP_CASE8(56)
-                UBQP_CASE8(64) UBQP_CASE8(72) UBQP_CASE8(80) UBQP_CASE8(88)
-                UBQP_CASE8(96) UBQP_CASE8(104) UBQP_CASE8(112) UBQP_CASE8(120)
+            switch (kstar / A::CHUNK) {
+                UBQP_CCASE(0) UBQP_CCASE(1) UBQP_CCASE(2) UBQP_CCASE(3)
+                UBQP_CCASE(4) UBQP_CCASE(5) UBQP_CCASE(6) UBQP_CCASE(7)
                 default: break;
             }
         }
@@ -370,8 +380,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         }
     }
 }
-#undef UBQP_CASE8
-#undef UBQP_CASE
+#undef UBQP_CCASE
 
 template <int BLOCK, int NCH>
 void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_t *f_dev,
