@@ -296,7 +296,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
                 k2 = dp2a_lo(a2, bhi, k2);
                 k3 = dp2a_hi(a2, bhi, k3);
                 if (c & 1) {
-                    if (wi & 1) {
+                    if (wi & 2) {
                         r6 = max(r6, max(k0, k1));
                         r7 = max(r7, max(k2, k3));
                     } else {
@@ -304,7 +304,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
                         r5 = max(r5, max(k2, k3));
                     }
                 } else {
-                    if (wi & 1) {
+                    if (wi & 2) {
                         r2 = max(r2, max(k0, k1));
                         r3 = max(r3, max(k2, k3));
                     } else {
