@@ -348,6 +348,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
+        "parity": None if args.no_parity else sampled_parity(cfg, Q, x0_bits, ms, m, rank, world),
     }
     if world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, Q)
@@ -394,6 +395,33 @@ def measure_int8_peak():
         return {"burst_tops": ops / best / 1e9, "sustained_tops": ops * cnt / e0.elapsed_time(e1) / 1e9}
     except Exception as exc:                                  # keep the bench line on failure
         return {"error": str(exc)[:200]} and None
+
+
+def sampled_parity(cfg, Q, x0_bits, ms, m, rank, world, samples=8):
+    """SURVEY §8(d) "sampled (>= 1024 g) for configs 4-5", bounded here to a few seconds:
+    survivors of the last timed step (first, last and random ones) are re-derived by the
+    oracle from their global index g -- Glover diversification, exact f, steepest ascent --
+    and compared exactly with the step's ascent outputs (f, flips, bits)."""
+    import oracle
+    from inputs import unpack_bits
+    if m == 0:
+        return {"checked": 0}
+    n = cfg["n"]
+    rng = np.random.default_rng(123)
+    pick = sorted({0, m - 1, *rng.integers(0, m, size=max(0, samples - 2)).tolist()})
+    surv = ms.surv[:m].cpu().numpy()
+    f_gpu = ms.f_asc[:m].cpu().numpy()
+    fl_gpu = ms.flips[:m].cpu().numpy()
+    b_gpu = unpack_bits(ms.bits[:m].cpu().numpy().view(np.uint64), n)
+    x0 = unpack_bits(x0_bits.cpu().numpy().view(np.uint64)[None, :], n)[0]
+    ok = 0
+    for i in pick:
+        g = rank + int(surv[i]) * world
+        X = oracle.diversify(x0, cfg.get("t0", 0) + g, 1)
+        Xa, fa, fla = oracle.ascend(Q, X, oracle.eval_batch(Q, X, os.cpu_count() or 1), cfg["max_flips"])
+        ok += int(fa[0] == f_gpu[i] and fla[0] == fl_gpu[i] and np.array_equal(Xa[0], b_gpu[i]))
+    return {"checked": len(pick), "exact": ok, "what": "survivors of the last timed step re-derived by the "
+            "oracle from g (diversify, eval, ascend): f, flips and bits compared exactly"}
 
 
 def cpu_baseline(cfg, Q):
@@ -626,6 +654,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-table1", action="store_true")
     ap.add_argument("--no-int8-peak", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the contract requires >= 3 warm-up steps", file=sys.stderr)
