@@ -10,7 +10,11 @@
  *     [caller all-reduces the stats across ranks]
  *     ubqp_screen                                     -> survivors of T(lambda)
  *     ubqp_ascend                                     -> 1-flip local optima + best key
+ * with, beyond that core: ubqp_blend (blend / breeding diversification),
+ * ubqp_relink (path relinking), and the real-valued Q path ubqp_load_Q_real /
+ * ubqp_eval_batch_real / ubqp_screen_real / ubqp_ascend_real.
  * Implemented by libubqp.so (paper_1706_00037_b200/csrc).  No torch types, no NCCL.
+ * ABI version 1.03 (ubqp_version() == 103).
  * Citations: P:n = PAPER.md line n (section in brackets), S:n = SPEC.md line n.
  *
  * Conventions (all calls)

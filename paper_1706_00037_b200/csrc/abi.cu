@@ -200,7 +200,7 @@ int check_batch_args(ubqp_t h, int64_t k_local, int32_t rank, int32_t world) {
 
 extern "C" {
 
-int ubqp_version(void) { return 100; }
+int ubqp_version(void) { return 103; }   // 1.03: + ubqp_blend, ubqp_relink, ubqp_ascend_real
 
 int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
     if (!out) return UBQP_E_INVALID;
