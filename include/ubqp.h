@@ -98,8 +98,8 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max);
  * loop counter").  For slot i, t = t0 + g (g = rank + i*world), taken mod n(n+1):
  *   h = floor((1 + isqrt(1 + 4t))/2), r = t - h(h-1), q = floor(r/2) + 1, c = r mod 2,
  *   x = seed xor {bits q-1, q-1+h, q-1+2h, ... < n}, complemented within n bits if c = 1.
- * seed_bits: W64 words.  Fills the handle's batch with k_local solutions (0 <= k_local
- * <= k_max).  Errors: E_INVALID, E_STATE (no Q). */
+ * seed_bits: W64 words; 0 <= t0 <= 2^62.  Fills the handle's batch with k_local solutions
+ * (0 <= k_local <= k_max).  Errors: E_INVALID, E_STATE (no Q). */
 int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_local,
                    int32_t rank, int32_t world);
 
@@ -128,7 +128,8 @@ int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank
 
 /* CalculateFirstDerivativeSolution (Figure 2; "simply sum the i^th row of Q
  * ... and if that sum is positive, then set x_i = 1"): bits_out[W64] gets x_i = 1 iff
- * sum_j Q_ij > 0.  Requires a loaded Q; does not touch the batch. */
+ * sum_j Q_ij > 0 (for a real-valued Q: the row sums of its fixed-point image, R20).
+ * Requires a loaded Q; does not touch the batch. */
 int ubqp_first_derivative(ubqp_t h, uint64_t *bits_out);
 
 /* Copy the current batch out: bits_out[k_local][W64]. */

@@ -341,7 +341,7 @@ int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_lo
     int rc = check_batch_args(h, k_local, rank, world);
     if (rc) return rc;
     if (!seed_bits) return fail(h, UBQP_E_INVALID, "ubqp: seed_bits is NULL");
-    if (t0 < 0) return fail(h, UBQP_E_INVALID, "ubqp: t0 < 0");
+    if (t0 < 0 || t0 > (1ll << 62)) return fail(h, UBQP_E_INVALID, "ubqp: t0 must be in [0, 2^62]");
     const uint64_t *seed_dev = seed_bits;
     if (!is_device_ptr(seed_bits)) {
         CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
@@ -363,7 +363,7 @@ int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int
     if (rc) return rc;
     if (!seed_bits || !parents) return fail(h, UBQP_E_INVALID, "ubqp: seed_bits or parents is NULL");
     if (n_parents < 1 || n_parents > (1ll << 22)) return fail(h, UBQP_E_INVALID, "ubqp: n_parents must be in [1, 2^22]");
-    if (t0 < 0) return fail(h, UBQP_E_INVALID, "ubqp: t0 < 0");
+    if (t0 < 0 || t0 > (1ll << 62)) return fail(h, UBQP_E_INVALID, "ubqp: t0 must be in [0, 2^62]");
     const uint64_t *seed_dev = seed_bits;
     if (!is_device_ptr(seed_bits)) {
         CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
