@@ -1,4 +1,4 @@
-// ascend.cu — K-ASC: batched steepest ascent on 1-bit flips (DESIGN.md §5.4).
+// ascend.cu — K-ASC: batched steepest ascent on 1-bit flips (DESIGN.md §7.4).
 //
 // PerformSteepestAscent ("terminating when no improvements are possible or
 // a maximum number of flips have been made. No checks for cycling nor tabu lists"), with
@@ -17,9 +17,12 @@
 // per element on FMA pipe: x is held as byte masks m (0xFF where x = 1), t = q ^ m is the
 // ones' complement of the negated bytes, and the (t_e, m_e) byte pairs dotted with
 // (C, -C) give C (t_e - m_e) = C s_e q_e exactly.  Per 4 elements and step: 1 LOP3 +
-// 2 PRMT + 2 IMNMX3 (ALU pipe) and 4 IDP.2A (FMA pipe).  The owner of k* pre-compensates K_k* through a jump table so the
-// fused loop needs no per-element test.  Argmax across lanes: __reduce_max/min_sync;
-// across warps: one __syncthreads over double-buffered shared slots.
+// 2 PRMT + 2 IMNMX3 (ALU pipe) and 4 IDP.2A (FMA pipe).  The owner of k* pre-compensates
+// K_k* through a two-level jump table (chunk, then element) so the fused loop needs no
+// per-element test.  Argmax across lanes: __reduce_max/min_sync; across warps: one
+// __syncthreads over double-buffered shared slots holding each warp's winner as one
+// orderable 64-bit word.  Codegen sits at the 168-register cap: A/B any edit on one box
+// (tools/ab.sh) -- DESIGN.md §13 lists the measured variants.
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
