@@ -1,4 +1,4 @@
-// eval_tc.cu — K-EVAL: batched xQx on 5th-generation tensor cores (DESIGN.md §5.2).
+// eval_tc.cu — K-EVAL: batched xQx on 5th-generation tensor cores (DESIGN.md §7.2).
 //
 // Y = X8 · Q8  (s8 x s8 -> s32, exact), never written to HBM: the accumulator tile lives
 // in TMEM and the epilogue folds it immediately into

@@ -1,4 +1,4 @@
-// gen.cu — K-GEN: on-device generation of the solution batch (DESIGN.md §5.1).
+// gen.cu — K-GEN: on-device generation of the solution batch (DESIGN.md §7.1).
 //
 // One thread per (slot, 64-bit word) of the padded row: it produces the packed word
 // Xb[slot][w] (w < W64) and its byte expansion X8[slot][64w .. 64w+63] (the int8
