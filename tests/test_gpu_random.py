@@ -1,6 +1,7 @@
 """Randomised GPU parity (hypothesis): arbitrary sizes, densities, coefficient ranges, seeds,
 lambda and max_flips; every output of eval / screen / ascent must equal the oracle exactly.
-UBQP_HYPO_EXAMPLES=N raises the example count of every test (long soak runs)."""
+UBQP_HYPO_EXAMPLES=N raises the example count of every test, UBQP_HYPO_NMAX the largest n
+(long soak runs over every ascent shape)."""
 import os
 
 import numpy as np
@@ -24,7 +25,7 @@ build_lib()
 
 
 @settings(max_examples=int(os.environ.get("UBQP_HYPO_EXAMPLES", 120)), deadline=None)
-@given(n=st.integers(1, 700), K=st.integers(1, 700), density=st.sampled_from([0.05, 0.3, 1.0]),
+@given(n=st.integers(1, int(os.environ.get("UBQP_HYPO_NMAX", 700))), K=st.integers(1, 700), density=st.sampled_from([0.05, 0.3, 1.0]),
        qmax=st.sampled_from([1, 7, 100, 127]), seed=st.integers(0, 2**31 - 1),
        lam=st.floats(-0.5, 1.5), max_flips=st.sampled_from([0, 1, 5, 10**6]),
        glover=st.booleans())
@@ -67,7 +68,7 @@ def test_round_matches_oracle(n, K, density, qmax, seed, lam, max_flips, glover)
 
 
 @settings(max_examples=int(os.environ.get("UBQP_HYPO_EXAMPLES", 60)), deadline=None)
-@given(n=st.integers(1, 600), K=st.integers(1, 300), P=st.integers(1, 9), qmax=st.sampled_from([1, 50, 127]),
+@given(n=st.integers(1, int(os.environ.get("UBQP_HYPO_NMAX", 600))), K=st.integers(1, 300), P=st.integers(1, 9), qmax=st.sampled_from([1, 50, 127]),
        seed=st.integers(0, 2**31 - 1), t0=st.integers(0, 10**6))
 def test_blend_and_relink_match_oracle(n, K, P, qmax, seed, t0):
     """O4b blend bits and O11 relinking outputs on arbitrary shapes (R11b, R19)."""
@@ -96,7 +97,7 @@ def test_blend_and_relink_match_oracle(n, K, P, qmax, seed, t0):
 
 
 @settings(max_examples=int(os.environ.get("UBQP_HYPO_EXAMPLES", 40)), deadline=None)
-@given(n=st.integers(1, 500), K=st.integers(1, 120), scale=st.sampled_from([1e-3, 1.0, 37.5, 1e6]),
+@given(n=st.integers(1, int(os.environ.get("UBQP_HYPO_NMAX", 500))), K=st.integers(1, 120), scale=st.sampled_from([1e-3, 1.0, 37.5, 1e6]),
        seed=st.integers(0, 2**31 - 1), f32=st.booleans(), max_flips=st.sampled_from([0, 3, 10**6]))
 def test_real_ascent_matches_oracle(n, K, scale, seed, f32, max_flips):
     """R20 real-Q ascent on arbitrary shapes and coefficient scales."""
