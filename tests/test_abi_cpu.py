@@ -87,3 +87,19 @@ def test_oracle_shares_no_code_with_the_cuda_path():
         if p.suffix in (".py", ".c", ".h"):
             for mod in _imports(p.read_text()):
                 assert not any(("paper_1706" in x or "ubqp.h" in x or "csrc" in x) for x in mod), (p, mod)
+
+
+def test_plain_c_example_compiles_against_the_header_and_library(tmp_path):
+    """The boundary is a C-ABI: a C99 program (examples/ubqp_round.c) compiles against
+    include/ubqp.h with -Wall -Wextra -Werror and links libubqp.so."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    from paper_1706_00037_b200.build import build_lib
+    build_lib()
+    out = tmp_path / "ubqp_round"
+    subprocess.check_call(["gcc", "-std=c99", "-O2", "-Wall", "-Wextra", "-Werror", f"-I{ROOT / 'include'}",
+                           str(ROOT / "examples" / "ubqp_round.c"), f"-L{ROOT / 'paper_1706_00037_b200'}", "-lubqp",
+                           f"-Wl,-rpath,{ROOT / 'paper_1706_00037_b200'}", "-o", str(out)])
+    assert out.exists()
