@@ -103,3 +103,11 @@ def test_plain_c_example_compiles_against_the_header_and_library(tmp_path):
                            str(ROOT / "examples" / "ubqp_round.c"), f"-L{ROOT / 'paper_1706_00037_b200'}", "-lubqp",
                            f"-Wl,-rpath,{ROOT / 'paper_1706_00037_b200'}", "-o", str(out)])
     assert out.exists()
+
+
+def test_binding_refuses_a_missing_library(tmp_path, monkeypatch):
+    """No CPU fallback: pointing the binding at a library that does not exist raises."""
+    import paper_1706_00037_b200.ubqp as ub
+    monkeypatch.setattr(ub, "_lib", None)      # restored by monkeypatch afterwards
+    with pytest.raises(OSError):
+        ub.load_library(tmp_path / "missing_libubqp.so")
