@@ -75,6 +75,9 @@ def main():
             kname = k["Kernel Name"][0]
             short = kname.split("(")[0].replace("void ", "").split("::")[-1].split("<")[0]
             lines += [f"## `{kname[:120]}`  ({rep.name})", "", "| metric | value |", "|---|---|"]
+            if "lts__t_bytes.sum" not in k and "lts__t_sectors.sum" in k:   # --set full has sectors
+                sv, _ = k["lts__t_sectors.sum"]
+                k["lts__t_bytes.sum"] = (f"{float(sv.replace(',', '')) * 32 / 1e9:.6f}", "Gbyte")
             for key, label in METRICS:
                 if key in k:
                     v, unit = k[key]
