@@ -19,7 +19,7 @@ namespace ubqp {
 namespace {
 
 constexpr int kRB = 256;                 // threads per solution
-constexpr long long kRPad = LLONG_MIN / 4;
+constexpr long long kRPad = LLONG_MIN / 2;   // padding / parked keys: never the maximum
 
 __global__ void __launch_bounds__(256) gains_combine_kernel(const int32_t *__restrict__ g32,
                                                             int64_t *__restrict__ g64,
@@ -63,20 +63,22 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
     uint64_t xm = 0;
     const int64_t *grow = g64 + s * n_pad;
     const uint64_t *xrow = Xb + s * W64;
-    long long bv = LLONG_MIN;
-    int bq = 0;
+    // stored as 64 Delta + (63 - q): one 64-bit max orders (gain, then lowest q)
+    long long bk = LLONG_MIN;
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
         const int j = t + kRB * q;
-        const long long g = j < n ? grow[j] : kRPad;
+        const long long g = j < n ? grow[j] * 64 + (63 - q) : kRPad;
         s_G[q * kRB + t] = g;
-        if (g > bv) { bv = g; bq = q; }
+        bk = max(bk, g);
         if (j < n) xm |= ((xrow[j >> 6] >> (j & 63)) & 1ull) << q;
     }
     long long fv = fint_in[s];
     int flips = 0;
     for (;;) {
         // ---- argmax: thread (tracked by the last update) -> warp (largest gain, then lowest j) -> block
+        const int bq = 63 - static_cast<int>(bk & 63);
+        long long bv = bk >> 6;
         unsigned bj = (static_cast<unsigned>(t + kRB * bq) << 1) | static_cast<unsigned>((xm >> bq) & 1ull);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -112,19 +114,19 @@ ascend_real_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         for (int q = 0; q < NPT; ++q) qv[q] = __ldg(row + kRB * q);   // rows padded to qt_ld
         // the owner parks Delta_k* out of reach of the max for the uniform pass, then stores -gv
         if (own >= 0) s_G[own * kRB + t] = kRPad;
-        const int c2 = static_cast<int>(d2);
-        bv = LLONG_MIN;
-        bq = 0;
+        const int c2 = static_cast<int>(d2) * 64;
+        bk = LLONG_MIN;
 #pragma unroll
         for (int q = 0; q < NPT; ++q) {
-            const int coef = ((xm >> q) & 1ull) ? -c2 : c2;           // 2 d (1 - 2 x_j)
+            const int coef = ((xm >> q) & 1ull) ? -c2 : c2;           // 64 * 2 d (1 - 2 x_j)
             const long long g = s_G[q * kRB + t] + static_cast<long long>(coef) * qv[q];   // IMAD.WIDE
             s_G[q * kRB + t] = g;
-            if (g > bv) { bv = g; bq = q; }
+            bk = max(bk, g);
         }
         if (own >= 0) {
-            s_G[own * kRB + t] = -gv;
-            if (-gv > bv || (-gv == bv && own < bq)) { bv = -gv; bq = own; }
+            const long long g = -gv * 64 + (63 - own);
+            s_G[own * kRB + t] = g;
+            bk = max(bk, g);
             xm ^= 1ull << own;
         }
     }
