@@ -57,3 +57,36 @@ def test_sharded_rounds_match_single_rank_oracle(world, div):
         assert best == obest and traj == otraj
         got = unpack_bits(np.frombuffer(bits, dtype=np.uint64)[None, :], n)[0]
         assert np.array_equal(got, ox)
+
+
+def _worker_real(rank, world, port, n, K, rounds, lam, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1706_00037_b200.multistart import MultiStartReal
+        rng = np.random.default_rng(n)
+        A = rng.uniform(-30, 30, size=(n, n))
+        Q = np.triu(A) + np.triu(A, 1).T
+        ms = MultiStartReal(Q, K, lam=lam, max_flips=10 * n, device=0)
+        best, bits, traj = ms.run(rounds, sample_seed=4)
+        out[rank] = (best, traj, bits.cpu().numpy().tobytes())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_real_rounds_match_single_rank_oracle():
+    """MultiStartReal (R20) on 2 ranks: int128 stats exchange, best (f~, g) record, owner bits."""
+    n, K, rounds, lam, world = 150, 900, 3, 0.35, 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker_real, args=(world, _port(), n, K, rounds, lam, out), nprocs=world, join=True)
+    rng = np.random.default_rng(n)
+    A = rng.uniform(-30, 30, size=(n, n))
+    Q = np.triu(A) + np.triu(A, 1).T
+    ob, ox, otraj, e = oracle.run_rounds_real(Q, K, rounds, lam, 10 * n, sample_seed=4, nthreads=8)
+    for r in range(world):
+        best, traj, bits = out[r]
+        assert best == ob and traj == otraj
+        assert np.array_equal(unpack_bits(np.frombuffer(bits, dtype=np.uint64)[None, :], n)[0], ox)
