@@ -271,6 +271,44 @@ def test_errors():
     assert st.count == 0 and st.max_key == -1
 
 
+def test_errors_of_every_call():
+    """Return codes of the C-ABI (include/ubqp.h "Errors"): each call rejects bad arguments
+    with its documented code and leaves the handle usable."""
+    u = Ubqp(0)
+    n = 70
+    Q = generate_Q(n, 0.5, seed=8)
+    codes = []
+
+    def err(fn, *a):
+        with pytest.raises(UbqpError) as e:
+            fn(*a)
+        codes.append(e.value.code)
+        return e.value.code
+
+    assert err(u.diversify, np.zeros(2, np.uint64), 0, 4) == 4           # no Q: E_STATE
+    assert err(u.load_Q, Q, 0) == 1                                    # k_max < 1
+    assert err(u.load_Q, Q, (1 << 22) + 1) == 1                        # k_max > 2^22
+    u.load_Q(Q, 64)
+    seed = pack_bits(oracle.first_derivative_start(Q))[0]
+    assert err(u.diversify, seed, -1, 8) == 1                          # t0 < 0
+    assert err(u.diversify, seed, (1 << 62) + 1, 8) == 1               # t0 > 2^62
+    assert err(u.blend, seed, pack_bits(np.zeros((1, n), np.uint8)), 1, -5, 8) == 1
+    assert err(u.diversify, seed, 0, 8, 3, 2) == 1                     # rank >= world
+    u.diversify(seed, 0, 8)
+    assert err(u.ascend, np.arange(8, dtype=np.int32), 8, 10) == 4     # not evaluated: E_STATE
+    u.eval_batch(UBQP_EMIT_GAINS)
+    surv = np.zeros(8, np.int32)
+    assert err(u.screen, float("nan"), 1, 1, 1, surv) == 1             # non-finite lambda
+    assert err(u.screen, 0.5, 1, 0, 1, surv) == 4                      # mean_count <= 0
+    assert err(u.ascend, np.arange(9, dtype=np.int32), 9, 10) == 1     # m > k_local
+    assert err(u.ascend, np.arange(8, dtype=np.int32), 8, -1) == 1     # max_flips < 0
+    assert err(u.get_gains, 5, 10, np.zeros((10, n), np.int32)) == 1   # slots past k_local
+    u.ascend(np.arange(8, dtype=np.int32), 8, 10)                      # still usable
+    assert err(u.ascend_real, np.arange(8, dtype=np.int32), 8, 10) == 4  # integer Q loaded
+    assert err(u.eval_batch_real) == 4
+    u.close()
+
+
 # ------------------------------------------------------------------ full-size, sampled
 @pytest.mark.parametrize("n,K,kind", [(5000, 1000, "random"), (7000, 1000, "random"),
                                       (7000, 262144, "glover")])
