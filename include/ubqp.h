@@ -14,7 +14,8 @@
  * ubqp_relink (path relinking), and the real-valued Q path ubqp_load_Q_real /
  * ubqp_eval_batch_real / ubqp_screen_real / ubqp_ascend_real.
  * Implemented by libubqp.so (paper_1706_00037_b200/csrc).  No torch types, no NCCL.
- * ABI version 1.03 (ubqp_version() == 103).
+ * ABI version 2.00 (ubqp_version() == 200): 2.00 widened ubqp_stats_real to int128 sums and
+ * maxima of an exact evaluation image and added ubqp_set_option.
  * Citations: P:n = PAPER.md line n (section in brackets), S:n = SPEC.md line n.
  *
  * Conventions (all calls)
@@ -128,7 +129,7 @@ int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank
 
 /* CalculateFirstDerivativeSolution (Figure 2; "simply sum the i^th row of Q
  * ... and if that sum is positive, then set x_i = 1"): bits_out[W64] gets x_i = 1 iff
- * sum_j Q_ij > 0 (for a real-valued Q: the row sums of its fixed-point image, R20).
+ * sum_j Q_ij > 0 (for a real-valued Q: the exact row sums of its evaluation image, R22).
  * Requires a loaded Q; does not touch the batch. */
 int ubqp_first_derivative(ubqp_t h, uint64_t *bits_out);
 
@@ -137,8 +138,8 @@ int ubqp_get_batch(ubqp_t h, uint64_t *bits_out);
 
 /* Evaluate (Figure 2 "xQx <- Evaluate(x)"; "the GPU, which excels at matrix
  * multiplication"): for every slot k of the batch, f_k = x_k^t Q x_k computed as
- * Y = X Q on int8 tensor cores (int32 exact) with the row-dot f_k = sum_j x_kj Y_kj
- * fused into the epilogue.  flags & UBQP_EMIT_GAINS additionally stores the 1-flip
+ * Y = X Q on int8 tensor cores (int32 exact) with the row-dot f_k = sum_j x_kj Y_kj and the
+ * statistics fused into the kernel (one launch; device f_out / stats_out are written by it).  flags & UBQP_EMIT_GAINS additionally stores the 1-flip
  * gains Delta_kj = Q_jj + 2(1 - 2 x_kj) Y_kj = f(x xor e_j) - f(x) on the device
  * for ubqp_ascend / ubqp_get_gains.  f_out: int64[k_local] (may be NULL); stats_out:
  * one ubqp_stats (may be NULL) = {sum f, k_local, max_key over the batch, 0}.
@@ -193,31 +194,52 @@ int ubqp_relink(ubqp_t h, const uint64_t *guides, int64_t n_guides, const int32_
 
 /* ---------------------------------------------------------------------------------
  * Real-valued Q (a4': "Q ... of real or integer coefficients"; "float or double",
- * P:89).  The coefficients are rounded once to 28-bit fixed point,
- *     Q~ = 2^-e round(Q 2^e),   e = max{e : max|Q_ij| 2^e <= 2^27 - 1},
- * and Q~ 2^e is stored as 4 int8 planes of balanced base-128 digits (|digit| <= 64), so each
- * plane runs through the same exact int8 tensor-core evaluation; f = 2^-e sum_s 128^s x^t L_s x
- * is the exact objective of Q~ (one final rounding to binary64).  Error bound:
- * |f - x^t Q x| <= |x|^2 2^-(e+1) (+ one binary64 rounding).  The ascent stays integer-only.
+ * P:89).  Two fixed-point images of Q are built at load (readings R20, R22):
+ *
+ *  - the EVALUATION image (R22) Qw = 2^-w rint(Q 2^w), with
+ *        w = max over nonzero Q_ij of min(lsb(Q_ij), 32 - ex(Q_ij)),
+ *    lsb(v) the least e making v 2^e an integer and |v| in [2^(ex-1), 2^ex): every coefficient
+ *    is EXACT, or (only possible for float64 input) at least 2^31 units of 2^-w, i.e. within
+ *    2^-32 |Q_ij|.  A float32 Q is always exact.  rint(Q 2^w) is stored as L <= 10 int8 planes
+ *    of balanced base-128 digits, each run through the exact int8 tensor-core evaluation;
+ *    f~ = x^t rint(Q 2^w) x is formed exactly (int128) and f = 2^-w f~ is rounded once to
+ *    binary64.  Error bound for every accepted Q and every x (S = {i : x_i = 1}):
+ *        |f - x^t Q x| <= 2^-32 sum_{i,j in S} |Q_ij| + 2^-53 |x^t Q x|
+ *                      <= 2^-32 |S| s(x) + 2^-53 |x^t Q x|,   s(x) = sqrt(sum_{i,j in S} Q_ij^2)
+ *    (Cauchy-Schwarz), so with |S| <= 16384: <= 3.9e-6 s(x) + 1.2e-16 |x^t Q x|, inside the
+ *    north_star tolerance 1e-5 max(|f|, s(x)) (reading R3).  For float32 Q the first term
+ *    vanishes: f is x^t Q x correctly rounded.  A Q needing more than 10 limbs (a dynamic
+ *    range max|Q| / min|Q_ij != 0| beyond about 2^36 with float64 significands) is rejected
+ *    with UBQP_E_RANGE.
+ *  - the WALK image (R20) Qt = rint(Q 2^e) (half-even), e the largest integer with
+ *    max|Q| 2^e <= 2^27 - 1 (ubqp_query UBQP_Q_REAL_EXP): the steepest ascent runs exactly on
+ *    it (int64 gains), so its flips are those of O7 on Qt; the returned f is then evaluated on
+ *    the evaluation image (bound above).
  * ------------------------------------------------------------------------------ */
 enum { UBQP_F32 = 1, UBQP_F64 = 2 };
 
-/* integer image statistics of a real-Q batch: f~_k = f_k 2^e (exact int64):
- * sum f~ as a two's-complement int128 (sum_hi:sum_lo), count, max f~ (INT64_MIN if empty). */
+/* statistics of a real-Q batch on the evaluation image, f~_k = f_k 2^exp exactly:
+ * sum f~ and max f~ as two's-complement int128 (hi:lo), count; max = INT128_MIN (hi =
+ * INT64_MIN, lo = 0) if the batch is empty.  48 bytes. */
 typedef struct {
     int64_t sum_hi;
-    int64_t sum_lo;
+    uint64_t sum_lo;
     int64_t count;
-    int64_t max_fint;
+    int64_t max_hi;
+    uint64_t max_lo;
+    int32_t exp;           /* w of the evaluation image: f = 2^-exp f~ */
+    int32_t reserved;      /* 0 */
 } ubqp_stats_real;
 
 /* Load a real-valued symmetric Q (row-major n*n float32 or float64, host or device).
- * Errors: E_NOT_SYMMETRIC, E_RANGE (non-finite), E_INVALID.  Replaces any earlier Q.
- * Batch generation calls work unchanged; integer-only calls return E_STATE. */
+ * Errors: E_NOT_SYMMETRIC, E_RANGE (non-finite coefficient, or more than 10 evaluation limbs
+ * needed), E_INVALID, E_NOMEM.  Replaces any earlier Q.  Batch generation calls work
+ * unchanged; integer-only calls return E_STATE.  Synchronises. */
 int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_max);
 
-/* Evaluate the batch against the real Q: f_out double[k_local] (may be NULL), stats_out
- * (may be NULL).  4 int8 tensor-core passes + an exact integer combine. */
+/* Evaluate the batch against the real Q (evaluation image, error bound above): f_out
+ * double[k_local] (may be NULL), stats_out (may be NULL).  One tensor-core launch over the
+ * L limb planes with the exact int128 combine and the statistics folded in-kernel. */
 int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out);
 
 /* Screen the last real batch: T = mean + lambda (max_value - mean) (binary64, no
@@ -227,13 +249,15 @@ int ubqp_screen_real(ubqp_t h, double lambda, double mean, double max_value, int
 
 /* Steepest ascent for real-valued Q (reading R20): ubqp_ascend's walk
  * (gains P:53; k* = argmax Delta, lowest j on ties; stop at Delta_k* <= 0
- * or max_flips) run exactly in int64 on the load-time fixed-point image
- * Qt = rint(Q 2^e) (half-even; e = ubqp_query(UBQP_Q_REAL_EXP), the largest integer with
- * max|Q| 2^e <= 2^27 - 1).  Starts: batch slots slots[i] of the last ubqp_eval_batch_real
- * (their int64 gains are formed here from the four int8 limb-plane GEMMs).  Outputs per i
- * (any may be NULL): f_out double[m] = 2^-e f~ (f~ = x^t Qt x of the local optimum, exact),
- * fint_out int64[m] = f~, flips_out int32[m], bits_out uint64[m][W64].  The batch is not
- * modified.  Memory: an int64 gains buffer of k_max * n_pad words on first use.
+ * or max_flips) run exactly in int64 on the walk image Qt = rint(Q 2^e) (e =
+ * ubqp_query(UBQP_Q_REAL_EXP)).  Starts: batch slots slots[i] of the last
+ * ubqp_eval_batch_real (their int64 gains are formed here from the four walk-image int8 limb
+ * planes).  Outputs per i (any may be NULL): f_out double[m] = f of the local optimum on the
+ * EVALUATION image (re-evaluated on the tensor cores; within the bound above of x^t Q x),
+ * fint_out int64[m] = x^t Qt x (the walk image, exact), flips_out int32[m], bits_out
+ * uint64[m][W64].  Every returned x is a 1-flip local optimum of Qt unless flips = max_flips;
+ * for the real Q its gains are then <= (2|S| + 1) 2^-(e+1).  The batch is not modified.
+ * Memory: int64 gains of k_max * n_pad words on first use.
  * Errors: E_STATE (no real Q / no evaluated real batch), E_INVALID, E_NOMEM, E_RANGE. */
 int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips,
                      double *f_out, int64_t *fint_out, int32_t *flips_out, uint64_t *bits_out);
@@ -241,10 +265,25 @@ int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flip
 /* Wait for all work queued on the handle's stream. */
 int ubqp_sync(ubqp_t h);
 
-/* Introspection (read-only): n, n_pad, W64, k_max, k_local, kernels launched so far. */
+/* Introspection (read-only): n, n_pad, W64, k_max, k_local, kernels launched so far, the
+ * stream, the walk-image exponent e (R20), 1 if a real Q is loaded, the evaluation-image
+ * exponent w and limb count L (R22; integer Q: 0 and 1), the off-diagonal nonzeros of an
+ * integer Q, 1 if its sparse rows (CSR, NEXT-3) were built (off-diagonal density <= 0.25). */
 enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
-       UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8 };
+       UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8,
+       UBQP_Q_EVAL_EXP = 9, UBQP_Q_EVAL_LIMBS = 10, UBQP_Q_NNZ = 11, UBQP_Q_SPARSE_ROWS = 12 };
 int ubqp_query(ubqp_t h, int what, int64_t *value);
+
+/* Kernel selection (results never depend on it; every choice is exact):
+ *   UBQP_OPT_ASCENT     0 = automatic (the sparse-row ascent when Q's off-diagonal density
+ *                       is at most the measured crossover and its rows were built), 1 = dense
+ *                       register ascent, 2 = sparse-row ascent (NEXT-3; E_STATE if the sparse
+ *                       rows were not built).  Used by ubqp_ascend.
+ *   UBQP_OPT_EVAL_PAIR  1 = CTA-pair (cta_group::2) evaluation (default), 0 = single CTA.
+ *   UBQP_OPT_EVAL_TRI   1 = f-only evaluations use the lower triangle of Q (default), 0 = full.
+ * Errors: E_INVALID (unknown option or value). */
+enum { UBQP_OPT_ASCENT = 0, UBQP_OPT_EVAL_PAIR = 1, UBQP_OPT_EVAL_TRI = 2 };
+int ubqp_set_option(ubqp_t h, int what, int64_t value);
 
 #ifdef __cplusplus
 }

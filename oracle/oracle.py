@@ -22,7 +22,7 @@ __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
     "first_derivative_start", "relink", "polish", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
-    "real_image", "ascend_real", "run_rounds_real",
+    "real_image", "ascend_real", "run_rounds_real", "gains_real", "batch_sum_exact",
 ]
 
 
@@ -380,42 +380,75 @@ def ascend_real(Q, X, max_flips: int, nthreads: int = 1):
     return Xa, fa, np.ldexp(fa.astype(np.float64), -e), fl, e
 
 
-# O8 on a real Q (R20): the batched rounds of run_rounds with every decision taken on the
-# fixed-point image Qt (sampling mean, first-derivative start, f~, T in binary64 on f = 2^-e f~)
+# O2 on a real Q: Delta_j = f(x xor e_j) - f(x) = (1 - 2 x_j)(Q_jj + 2 sum_{i != j, x_i = 1} Q_ij)
+# (S:164), each gain the exactly rounded sum of its terms (math.fsum; +-2 Q_ij is exact
+# in binary64).  Independent of any fixed-point image.
+def gains_real(Q, x) -> np.ndarray:
+    import math
+    Q = np.asarray(Q, dtype=np.float64)
+    x = np.asarray(x).reshape(-1).astype(bool)
+    S = np.flatnonzero(x)
+    out = np.empty(Q.shape[0], dtype=np.float64)
+    for j in range(Q.shape[0]):
+        d = -1.0 if x[j] else 1.0
+        terms = [d * Q[j, j]] + [2.0 * d * Q[i, j] for i in S if i != j]
+        out[j] = math.fsum(terms)
+    return out
+
+
+def batch_sum_exact(Q, X):
+    """sum_k x_k^t Q x_k as an exact rational (fractions.Fraction): sum_ij Q_ij c_ij with the
+    integer co-occurrence counts c = X^t X (a library matmul of 0/1 matrices)."""
+    from fractions import Fraction
+    Q = np.asarray(Q, dtype=np.float64)
+    X = np.asarray(X, dtype=np.int64)
+    C = X.T @ X
+    tot = Fraction(0)
+    for q, c in zip(Q.ravel().tolist(), C.ravel().tolist()):
+        if q != 0.0 and c:
+            tot += Fraction(q) * c
+    return tot
+
+
+# O8 on a real Q (R20, R22): the batched rounds of run_rounds where every objective value is
+# the exactly rounded x^t Q x (O9) and each survivor's walk is O7 on the walk image Qt (O9b)
 def run_rounds_real(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
                     world: int = 1, nthreads: int = 1):
-    """Returns (best f~ int, best x, trajectory [(round, f~)], e).  Mean = 2^-e (sum f~ / K)
-    (one correctly rounded division), Max = 2^-e max(incumbent, batch max),
-    T = Mean + lam (Max - Mean) in binary64, survivors f > T, incumbent replaced iff the
-    best ascended f~ is strictly greater (ties: lowest g)."""
-    import math
+    """Round 0: K random starts (O3); Mean = the exact rational mean of their objective values,
+    rounded once to binary64 (the pinned sampling mean; R5).  Incumbent = the
+    first-derivative start on the exactly rounded row sums, value O9.  Round r >= 1:
+    Glover diversification with t0 = (r-1)K (O4); f = O9 of each; Max = max(incumbent, batch
+    max) (R6); T = Mean + lam (Max - Mean) in binary64; survivors f > T; each
+    survivor walks O7 on Qt = rint(Q 2^e) (R20) and its final x is valued by O9; the incumbent
+    is replaced iff the best value is strictly greater, ties to the lowest g (R8, R14).
+    Returns (best f, best x, trajectory [(round, f)], e)."""
+    Q = np.asarray(Q, dtype=np.float64)
     Qt, e = real_image(Q)
     Qi = Qt.astype(np.int32)
-    n = Qi.shape[0]
-    mean_sum = 0
+    n = Q.shape[0]
+    from fractions import Fraction
+    total = Fraction(0)
     for r in range(world):
-        mean_sum += int(eval_batch(Qi, random_solutions(n, sample_seed, len(range(r, K, world)), r, world),
-                                   nthreads).sum())
-    mean = math.ldexp(mean_sum / K, -e)
-    inc_x = first_derivative_start(Qi)
-    inc_f = xQx(Qi, inc_x)
+        total += batch_sum_exact(Q, random_solutions(n, sample_seed, len(range(r, K, world)), r, world))
+    mean = float(total / K)
+    inc_x = first_derivative_start_real(Q)
+    inc_f = xQx_real(Q, inc_x)
     traj = [(0, inc_f)]
     for rnd in range(1, rounds + 1):
         t0 = (rnd - 1) * K
         Xs = [diversify(inc_x, t0, len(range(r, K, world)), r, world) for r in range(world)]
-        fs = [eval_batch(Qi, Xr, nthreads) for Xr in Xs]
-        bmax = max(int(fr.max()) for fr in fs if fr.size)
-        maxv = math.ldexp(float(max(inc_f, bmax)), -e)
+        fs = [eval_batch_real(Q, Xr) for Xr in Xs]
+        bmax = max(float(fr.max()) for fr in fs if fr.size)
+        maxv = max(inc_f, bmax)
         T = mean + lam * (maxv - mean)
         best = None
         for r in range(world):
-            fr = np.ldexp(fs[r].astype(np.float64), -e)
-            s = np.flatnonzero(fr > T)
+            s = np.flatnonzero(fs[r] > T)
             if s.size == 0:
                 continue
-            Xa, fa, _ = ascend(Qi, Xs[r][s], fs[r][s], max_flips, nthreads)
+            Xa, _, _ = ascend(Qi, Xs[r][s], eval_batch(Qi, Xs[r][s], nthreads), max_flips, nthreads)
             for i, slot in enumerate(s):
-                cand = (int(fa[i]), -(r + int(slot) * world))
+                cand = (xQx_real(Q, Xa[i]), -(r + int(slot) * world))
                 if best is None or cand > best[0]:
                     best = (cand, Xa[i].copy())
         if best is not None and best[0][0] > inc_f:

@@ -4,6 +4,8 @@
 // in binary64 and marshals arguments.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -73,6 +75,8 @@ void dfree(T *&p) {
 void free_batch(Ctx &c) {
     dfree(c.Xb); dfree(c.X8); dfree(c.f); dfree(c.gains); dfree(c.surv); dfree(c.blk_count);
     dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots); dfree(c.asc_aux);
+    dfree(c.part); dfree(c.grp_cnt); dfree(c.grp_res); dfree(c.X8r);
+    c.part_cap = c.grp_cap = 0;
     c.asc_cap = 0;
     c.k_max = 0; c.k_cap_pad = 0; c.k_local = -1;
     c.f_valid = c.gains_valid = c.gains64_valid = false;
@@ -81,13 +85,19 @@ void free_batch(Ctx &c) {
 void free_all(Ctx &c) {
     free_batch(c);
     dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents); dfree(c.guides);
+    dfree(c.csr_ptr); dfree(c.csr_ent);
+    c.nnz = 0;
     c.parents_cap = c.guides_cap = 0; dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
+    for (int s = 0; s < ubqp::kMaxLimbs; ++s) { dfree(c.Qw[s]); dfree(c.QwL[s]); }
+    dfree(c.wdiag); dfree(c.zdiag);
     dfree(c.fs); dfree(c.fint); dfree(c.freal); dfree(c.Qt); dfree(c.diagt); dfree(c.gains64);
+    c.op_full = c.op_tri = c.op_wide = ubqp::Operand{};
+    for (auto &o : c.op_walk) o = ubqp::Operand{};
     c.qt_ld = 0;
     c.real = false;
     c.freal_valid = false;
-    c.q_exp = 0;
+    c.q_exp = c.w_exp = c.w_limbs = 0;
     c.n = 0;
 }
 
@@ -120,6 +130,94 @@ bool encode_map(CUtensorMap *m, void *base, uint64_t cols, uint64_t rows, uint32
     return r == CUDA_SUCCESS;
 }
 
+// B operand from int8 planes [rows][ld] (plane s weighs 128^s): 256-row and 128-row boxes
+bool set_operand(ubqp::Operand &op, int8_t *const *planes, int count, uint64_t ld, bool tri,
+                 const int32_t *const *diag, int n_pad, int q_rows) {
+    op = ubqp::Operand{};
+    op.planes = count;
+    op.tri = tri;
+    for (int s = 0; s < count; ++s) {
+        if (!encode_map(&op.full[s], planes[s], n_pad, q_rows, ubqp::kBN, ld) ||
+            !encode_map(&op.half[s], planes[s], n_pad, q_rows, ubqp::kBN / 2, ld))
+            return false;
+        op.diag[s] = diag[s];
+    }
+    return true;
+}
+
+// grow the in-kernel fold buffers for a launch of this shape (synchronises when growing;
+// new counters start at zero and reset themselves after every launch)
+int ensure_fold(ubqp_t h, const ubqp::EvalShape &s) {
+    if (s.part_elems > h->part_cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(h->part);
+        h->part_cap = 0;
+        if (cudaMalloc(&h->part, s.part_elems * sizeof(int32_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the evaluation partials");
+        }
+        h->part_cap = s.part_elems;
+    }
+    if (s.num_groups + 1 > h->grp_cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        dfree(h->grp_cnt);
+        dfree(h->grp_res);
+        h->grp_cap = 0;
+        const int64_t cap = s.num_groups + 1;
+        if (cudaMalloc(&h->grp_cnt, cap * sizeof(unsigned)) != cudaSuccess ||
+            cudaMalloc(&h->grp_res, cap * 4 * sizeof(int64_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the evaluation counters");
+        }
+        CK(cudaMemsetAsync(h->grp_cnt, 0, cap * sizeof(unsigned), h->stream));
+        h->grp_cap = cap;
+    }
+    return UBQP_OK;
+}
+
+// one evaluation launch (sizes the fold buffers first)
+int eval_launch(ubqp_t h, const ubqp::EvalLaunch &L) {
+    if (L.k <= 0) return UBQP_OK;
+    const ubqp::EvalShape s = ubqp::eval_shape(*h, L.k, L.op->planes, L.emit_gains, L.op->tri && !L.emit_gains);
+    int rc = ensure_fold(h, s);
+    if (rc) return rc;
+    if (ubqp::launch_eval(*h, L)) return fail(h, UBQP_E_CUDA, "ubqp: evaluation fold buffers too small");
+    CK_LAUNCH("eval_tc kernel");
+    return UBQP_OK;
+}
+
+// CSR rows of Q without the diagonal for the sparse ascent (NEXT-3), built when the
+// off-diagonal density is at most kSparseBuildDensity; entries (j << 8) | (Q_kj & 0xFF), j ascending
+constexpr double kSparseBuildDensity = 0.25;
+int build_sparse(ubqp_t h, const int32_t *Qh) {
+    const int n = h->n;
+    int64_t nnz = 0;
+    for (int64_t e = 0; e < static_cast<int64_t>(n) * n; ++e) nnz += Qh[e] != 0;
+    for (int i = 0; i < n; ++i) nnz -= Qh[static_cast<int64_t>(i) * n + i] != 0;
+    h->nnz = nnz;
+    if (n < 2 || static_cast<double>(nnz) > kSparseBuildDensity * n * (n - 1.0)) return UBQP_OK;
+    std::vector<int32_t> ptr(n + 1, 0);
+    std::vector<uint32_t> ent(nnz > 0 ? nnz : 1);
+    int64_t at = 0;
+    for (int i = 0; i < n; ++i) {
+        ptr[i] = static_cast<int32_t>(at);
+        for (int j = 0; j < n; ++j) {
+            const int32_t v = Qh[static_cast<int64_t>(i) * n + j];
+            if (j != i && v != 0) ent[at++] = (static_cast<uint32_t>(j) << 8) | (static_cast<uint32_t>(v) & 0xFFu);
+        }
+    }
+    ptr[n] = static_cast<int32_t>(at);
+    if (cudaMalloc(&h->csr_ptr, ptr.size() * sizeof(int32_t)) != cudaSuccess ||
+        cudaMalloc(&h->csr_ent, ent.size() * sizeof(uint32_t)) != cudaSuccess) {
+        cudaGetLastError();
+        free_all(*h);
+        return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the sparse rows of Q");
+    }
+    CK(cudaMemcpy(h->csr_ptr, ptr.data(), ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->csr_ent, ent.data(), ent.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    return UBQP_OK;
+}
+
 int ensure_gains(ubqp_t h) {
     if (h->gains) return UBQP_OK;
     size_t bytes = static_cast<size_t>(h->k_max) * h->n_pad * sizeof(int32_t);
@@ -149,6 +247,16 @@ int ensure_asc(ubqp_t h, int64_t m) {
     return UBQP_OK;
 }
 
+// host -> device copy on the handle's stream, then wait: a pinned source copies truly
+// asynchronously, and include/ubqp.h promises that the call synchronises when it reads a
+// host array, so the caller may reuse or free it as soon as the call returns.
+int h2d_sync(ubqp_t h, void *dst, const void *src, size_t bytes) {
+    if (!bytes) return UBQP_OK;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return UBQP_OK;
+}
+
 // stage rows*W64 packed words on the device (device pointers pass through)
 int stage_rows(ubqp_t h, const uint64_t *src, int64_t rows, uint64_t *&buf, int64_t &cap, const uint64_t *&out) {
     if (is_device_ptr(src)) {
@@ -165,23 +273,42 @@ int stage_rows(ubqp_t h, const uint64_t *src, int64_t rows, uint64_t *&buf, int6
         }
         cap = rows;
     }
-    CK(cudaMemcpyAsync(buf, src, rows * h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+    const int rc = h2d_sync(h, buf, src, rows * h->W64 * sizeof(uint64_t));
+    if (rc) return rc;
     out = buf;
     return UBQP_OK;
 }
 
-// run the evaluation GEMM (+ stats into scratch64[0..3]) on the current batch
-int run_eval(ubqp_t h, bool emit_gains) {
+// run the evaluation GEMM on the current batch: f (+ gains) and the stats {sum, K, max_key, 0}
+// folded in-kernel into h->f / scratch64[0..3] and, when given, device copies f_dev / stats_dev
+int run_eval(ubqp_t h, bool emit_gains, int64_t *f_dev = nullptr, int64_t *stats_dev = nullptr) {
     if (emit_gains) {
         int rc = ensure_gains(h);
         if (rc) return rc;
     }
     const int64_t k = h->k_local;
-    if (k > 0) CK(cudaMemsetAsync(h->f, 0, k * sizeof(int64_t), h->stream));
-    ubqp::launch_eval_tc(*h, k, emit_gains, -1, nullptr, h->sym_eval && h->Q8L && !emit_gains);
-    CK_LAUNCH("eval_tc_kernel");
-    ubqp::launch_stats(*h, k, h->scratch64);
-    CK_LAUNCH("stats_kernel");
+    if (k == 0) {   // empty batch: the stats of nothing
+        const int64_t z[4] = {0, 0, -1, 0};
+        CK(cudaMemcpyAsync(h->scratch64, z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+        if (stats_dev) CK(cudaMemcpyAsync(stats_dev, z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));   // z is a stack array
+    } else {
+        ubqp::EvalLaunch L;
+        L.tmX = &h->tmap_X8;
+        L.Xb = h->Xb;
+        L.k = k;
+        L.op = (h->sym_eval && !emit_gains) ? &h->op_tri : &h->op_full;
+        L.emit_gains = emit_gains;
+        L.mode = ubqp::kFoldInt;
+        L.f = h->f;
+        L.f2 = f_dev;
+        L.stats = h->scratch64;
+        L.stats2 = stats_dev;
+        L.rank = h->rank;
+        L.world = h->world;
+        const int rc = eval_launch(h, L);
+        if (rc) return rc;
+    }
     h->f_valid = true;
     h->gains_valid = emit_gains;
     return UBQP_OK;
@@ -200,7 +327,7 @@ int check_batch_args(ubqp_t h, int64_t k_local, int32_t rank, int32_t world) {
 
 extern "C" {
 
-int ubqp_version(void) { return 103; }   // 1.03: + ubqp_blend, ubqp_relink, ubqp_ascend_real
+int ubqp_version(void) { return 200; }   // 2.00: int128 real-Q stats of the evaluation image, ubqp_set_option
 
 int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
     if (!out) return UBQP_E_INVALID;
@@ -233,7 +360,7 @@ int ubqp_create(int device, void *cuda_stream, ubqp_t *out) {
         }
         h->own_stream = true;
     }
-    if (cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)) != cudaSuccess) {
+    if (cudaMalloc(&h->scratch64, 32 * sizeof(int64_t)) != cudaSuccess) {
         if (h->own_stream) cudaStreamDestroy(h->stream);
         delete h;
         return UBQP_E_NOMEM;
@@ -265,8 +392,10 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
     std::vector<int32_t> hq;
     const int32_t *Qh = Q;
     if (is_device_ptr(Q)) {
+        // ordered after the caller's work on the handle's stream (Q may have just been written there)
         hq.resize(nn);
-        CK(cudaMemcpy(hq.data(), Q, nn * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(hq.data(), Q, nn * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
         Qh = hq.data();
     }
     for (int i = 0; i < n; ++i)
@@ -278,7 +407,7 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
         }
     CK(cudaStreamSynchronize(h->stream));
     free_all(*h);
-    CK(cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)));
+    CK(cudaMalloc(&h->scratch64, 32 * sizeof(int64_t)));
     h->n = n;
     h->n_pad = (n + ubqp::kNPadAlign - 1) / ubqp::kNPadAlign * ubqp::kNPadAlign;
     h->q_rows = (n + ubqp::kQRowAlign - 1) / ubqp::kQRowAlign * ubqp::kQRowAlign;
@@ -322,13 +451,17 @@ int ubqp_load_Q(ubqp_t h, int32_t n, const int32_t *Q, int64_t k_max) {
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the batch workspace");
     }
     CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
+    int8_t *full_pl[1] = {h->Q8}, *tri_pl[1] = {h->Q8L};
+    const int32_t *dg_pl[1] = {h->diag};
     if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM) ||
-        !encode_map(&h->tmap_Q8, h->Q8, h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
-        !encode_map(&h->tmap_Q8L, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN) ||
-        !encode_map(&h->tmap_Q8_h, h->Q8, h->n_pad, h->q_rows, ubqp::kBN / 2, h->q_ld) ||
-        !encode_map(&h->tmap_Q8L_h, h->Q8L, h->n_pad, h->q_rows, ubqp::kBN / 2)) {
+        !set_operand(h->op_full, full_pl, 1, h->q_ld, false, dg_pl, h->n_pad, h->q_rows) ||
+        !set_operand(h->op_tri, tri_pl, 1, h->n_pad, true, dg_pl, h->n_pad, h->q_rows)) {
         free_all(*h);
         return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
+    }
+    {
+        int rc2 = build_sparse(h, Qh);
+        if (rc2) return rc2;
     }
     h->k_local = -1;
     CK(cudaDeviceSynchronize());
@@ -344,7 +477,8 @@ int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_lo
     if (t0 < 0 || t0 > (1ll << 62)) return fail(h, UBQP_E_INVALID, "ubqp: t0 must be in [0, 2^62]");
     const uint64_t *seed_dev = seed_bits;
     if (!is_device_ptr(seed_bits)) {
-        CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+        const int rc2 = h2d_sync(h, h->seed, seed_bits, h->W64 * sizeof(uint64_t));
+        if (rc2) return rc2;
         seed_dev = h->seed;
     }
     h->rank = rank;
@@ -366,7 +500,8 @@ int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int
     if (t0 < 0 || t0 > (1ll << 62)) return fail(h, UBQP_E_INVALID, "ubqp: t0 must be in [0, 2^62]");
     const uint64_t *seed_dev = seed_bits;
     if (!is_device_ptr(seed_bits)) {
-        CK(cudaMemcpyAsync(h->seed, seed_bits, h->W64 * sizeof(uint64_t), cudaMemcpyHostToDevice, h->stream));
+        const int rc2 = h2d_sync(h, h->seed, seed_bits, h->W64 * sizeof(uint64_t));
+        if (rc2) return rc2;
         seed_dev = h->seed;
     }
     const uint64_t *par_dev = nullptr;
@@ -401,8 +536,12 @@ int ubqp_set_batch(ubqp_t h, const uint64_t *bits, int64_t k_local, int32_t rank
     if (!bits && k_local > 0) return fail(h, UBQP_E_INVALID, "ubqp: bits is NULL");
     const size_t bytes = static_cast<size_t>(k_local) * h->W64 * sizeof(uint64_t);
     if (bytes) {
-        CK(cudaMemcpyAsync(h->Xb, bits, bytes, is_device_ptr(bits) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                           h->stream));
+        if (is_device_ptr(bits)) {
+            CK(cudaMemcpyAsync(h->Xb, bits, bytes, cudaMemcpyDeviceToDevice, h->stream));
+        } else {
+            rc = h2d_sync(h, h->Xb, bits, bytes);
+            if (rc) return rc;
+        }
     }
     h->rank = rank;
     h->world = world;
@@ -448,21 +587,21 @@ int ubqp_eval_batch(ubqp_t h, int flags, int64_t *f_out, ubqp_stats *stats_out) 
     if (h->real) return fail(h, UBQP_E_STATE, "ubqp: real-valued Q loaded: use ubqp_eval_batch_real");
     if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch to evaluate");
     if (flags & ~UBQP_EMIT_GAINS) return fail(h, UBQP_E_INVALID, "ubqp: unknown flags");
-    int rc = run_eval(h, (flags & UBQP_EMIT_GAINS) != 0);
+    const int64_t k = h->k_local;
+    // device outputs are written by the kernel itself (one launch); host outputs are copied
+    const bool f_dev = f_out && is_device_ptr(f_out);
+    const bool s_dev = stats_out && is_device_ptr(stats_out);
+    int rc = run_eval(h, (flags & UBQP_EMIT_GAINS) != 0, f_dev ? f_out : nullptr,
+                      s_dev ? reinterpret_cast<int64_t *>(stats_out) : nullptr);
     if (rc) return rc;
     bool sync = false;
-    const int64_t k = h->k_local;
-    if (f_out && k > 0) {
-        const bool dev = is_device_ptr(f_out);
-        CK(cudaMemcpyAsync(f_out, h->f, k * sizeof(int64_t), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                           h->stream));
-        sync |= !dev;
+    if (f_out && !f_dev && k > 0) {
+        CK(cudaMemcpyAsync(f_out, h->f, k * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
     }
-    if (stats_out) {
-        const bool dev = is_device_ptr(stats_out);
-        CK(cudaMemcpyAsync(stats_out, h->scratch64, sizeof(ubqp_stats),
-                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
-        sync |= !dev;
+    if (stats_out && !s_dev) {
+        CK(cudaMemcpyAsync(stats_out, h->scratch64, sizeof(ubqp_stats), cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
     }
     if (sync) CK(cudaStreamSynchronize(h->stream));
     return UBQP_OK;
@@ -504,7 +643,7 @@ int ubqp_screen(ubqp_t h, double lambda, int64_t mean_sum, int64_t mean_count, i
     else if (fl < -9.2233720368547758e18) t_floor = INT64_MIN;
     else t_floor = static_cast<int64_t>(fl);
     const int64_t k = h->k_local;
-    ubqp::launch_screen(*h, k, t_floor, h->scratch64 + 4);
+    CK(ubqp::launch_screen(*h, k, t_floor, h->scratch64 + 4));
     CK_LAUNCH("screen kernels");
     int64_t m = 0;
     CK(cudaMemcpyAsync(&m, h->scratch64 + 4, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
@@ -539,7 +678,8 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, in
     if (m > 0 && !is_device_ptr(slots)) {
         for (int64_t i = 0; i < m; ++i)
             if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
-        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        const int rc2 = h2d_sync(h, h->asc_slots, slots, m * sizeof(int32_t));
+        if (rc2) return rc2;
         slots_dev = h->asc_slots;
     }
     const bool f_dev = f_out && is_device_ptr(f_out);
@@ -592,7 +732,8 @@ int ubqp_relink(ubqp_t h, const uint64_t *guides, int64_t n_guides, const int32_
     if (m > 0 && !is_device_ptr(slots)) {
         for (int64_t i = 0; i < m; ++i)
             if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
-        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        const int rc2 = h2d_sync(h, h->asc_slots, slots, m * sizeof(int32_t));
+        if (rc2) return rc2;
         slots_dev = h->asc_slots;
     }
     const bool f_dev = f_out && is_device_ptr(f_out);
@@ -627,6 +768,48 @@ int ubqp_relink(ubqp_t h, const uint64_t *guides, int64_t n_guides, const int32_
 }
 
 // ---------------------------------------------------------------- real-valued Q (a4')
+}  // extern "C"
+
+namespace {
+
+// R22: exponent of one nonzero coefficient v, |v| = fr 2^ex (fr in [1/2, 1)): the least e
+// making v 2^e an integer, capped at 32 - ex, where |v| 2^e >= 2^31 so rounding costs at most
+// 2^-32 of |v|.  A float32 coefficient never reaches the cap (24-bit significand): exact.
+int coeff_exp(double v, int &ex_out) {
+    int ex = 0;
+    const double fr = std::frexp(std::fabs(v), &ex);
+    const uint64_t M = static_cast<uint64_t>(std::ldexp(fr, 53));   // exact 53-bit integer
+    const int tz = __builtin_ctzll(M);
+    ex_out = ex;
+    return std::min(53 - ex - tz, 32 - ex);
+}
+
+// rint(v 2^e) (half to even), exact, for |v 2^e| < 2^100
+__int128 scaled_int(double v, int e) {
+    if (v == 0.0) return 0;
+    int ex = 0;
+    const double fr = std::frexp(std::fabs(v), &ex);
+    const uint64_t M = static_cast<uint64_t>(std::ldexp(fr, 53));
+    const int sh = ex - 53 + e;
+    unsigned __int128 r;
+    if (sh >= 0) {
+        r = static_cast<unsigned __int128>(M) << sh;
+    } else {
+        const int d = -sh;
+        if (d > 63) {
+            r = 0;   // |v 2^e| < 2^-10: rounds to 0 (cannot happen for e >= e_v, kept for safety)
+        } else {
+            const uint64_t q = M >> d, rem = M & ((1ull << d) - 1ull), half = 1ull << (d - 1);
+            r = q + ((rem > half || (rem == half && (q & 1ull))) ? 1u : 0u);
+        }
+    }
+    return v < 0 ? -static_cast<__int128>(r) : static_cast<__int128>(r);
+}
+
+}  // namespace
+
+extern "C" {
+
 int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_max) {
     GUARD(h);
     if (!Q || n < 1 || n > 16384) return fail(h, UBQP_E_INVALID, "ubqp: n must be in [1, 16384]");
@@ -638,7 +821,8 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
     const void *Qh = Q;
     if (is_device_ptr(Q)) {
         raw.resize(nn * esz);
-        CK(cudaMemcpy(raw.data(), Q, nn * esz, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(raw.data(), Q, nn * esz, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
         Qh = raw.data();
     }
     auto at = [&](int64_t idx) -> double {
@@ -646,15 +830,21 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
                                  : static_cast<const double *>(Qh)[idx];
     };
     double amax = 0.0;
+    int e_w = INT_MIN, ex_max = INT_MIN;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
             const double v = at(static_cast<int64_t>(i) * n + j);
             if (!std::isfinite(v)) return fail(h, UBQP_E_RANGE, "ubqp: non-finite coefficient");
             if (j > i && v != at(static_cast<int64_t>(j) * n + i))
                 return fail(h, UBQP_E_NOT_SYMMETRIC, "ubqp: Q is not symmetric");
+            if (v != 0.0) {
+                int ex = 0;
+                e_w = std::max(e_w, coeff_exp(v, ex));
+                ex_max = std::max(ex_max, ex);
+            }
             amax = std::fabs(v) > amax ? std::fabs(v) : amax;
         }
-    // 28-bit fixed point: |round(Q 2^e)| <= 2^27 - 1 = the range of 4 balanced base-128 limbs
+    // walk image (R20): 28-bit fixed point, |rint(Q 2^e)| <= 2^27 - 1 (four balanced base-128 limbs)
     int e = 0;
     if (amax > 0) {
         e = static_cast<int>(std::floor(std::log2((134217727.0) / amax)));
@@ -662,23 +852,48 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
         while (std::ldexp(amax, e + 1) <= 134217727.0 && e < 1000) ++e;
     }
     if (e < -900 || e > 900) return fail(h, UBQP_E_RANGE, "ubqp: coefficient scale out of range");
+    // evaluation image (R22): exponent e_w, limbs L with max|rint(Q 2^e_w)| <= 126 * 128^(L-1)
+    if (e_w == INT_MIN) e_w = 0;   // Q = 0
+    int limbs = 1;
+    if (ex_max != INT_MIN && ex_max + e_w > 7 * ubqp::kMaxLimbs) {
+        limbs = ubqp::kMaxLimbs + 1;   // |V| >= 2^70: beyond any admissible limb count
+    } else if (amax > 0) {
+        // balanced digits: the lower L-1 digits lie in [-64, 63], so the top one stays within
+        // int8 when max|V| <= 126 * 128^(L-1) (L = 1: the value itself, <= 127)
+        const __int128 vmax = scaled_int(amax, e_w);
+        __int128 cap = 127;
+        while (limbs <= ubqp::kMaxLimbs && vmax > cap) {
+            ++limbs;
+            cap = static_cast<__int128>(126) << (7 * (limbs - 1));
+        }
+    }
+    if (limbs > ubqp::kMaxLimbs || e_w < -900 || e_w > 900)
+        return fail(h, UBQP_E_RANGE,
+                    "ubqp: coefficient dynamic range too wide: the evaluation image would need more than 10 int8 "
+                    "limb planes (70 bits; DESIGN.md R22)");
     CK(cudaStreamSynchronize(h->stream));
     free_all(*h);
-    CK(cudaMalloc(&h->scratch64, 16 * sizeof(int64_t)));
+    CK(cudaMalloc(&h->scratch64, 32 * sizeof(int64_t)));
     h->n = n;
     h->n_pad = (n + ubqp::kNPadAlign - 1) / ubqp::kNPadAlign * ubqp::kNPadAlign;
     h->q_rows = (n + ubqp::kQRowAlign - 1) / ubqp::kQRowAlign * ubqp::kQRowAlign;
     h->W64 = (n + 63) / 64;
     h->real = true;
     h->q_exp = e;
+    h->w_exp = e_w;
+    h->w_limbs = limbs;
     h->q_ld = ubqp::ascend_capacity(h->n_pad);
     const size_t plane = static_cast<size_t>(h->q_rows) * h->q_ld;
+    const size_t tplane = static_cast<size_t>(h->q_rows) * h->n_pad;
     std::vector<int8_t> L(plane * ubqp::kSlices, 0);
+    std::vector<int8_t> W(plane * limbs, 0), WL(tplane * limbs, 0);
+    std::vector<int32_t> wdg(static_cast<size_t>(ubqp::kMaxLimbs) * h->q_rows, 0);
     h->qt_ld = ubqp::real_qt_ld(h->n_pad);
     std::vector<int32_t> qt(static_cast<size_t>(h->q_rows) * h->qt_ld, 0), dgt(h->n_pad, 0);
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) {
-            long long v = std::llrint(std::ldexp(at(static_cast<int64_t>(i) * n + j), e));
+            const double q = at(static_cast<int64_t>(i) * n + j);
+            long long v = std::llrint(std::ldexp(q, e));
             qt[static_cast<size_t>(i) * h->qt_ld + j] = static_cast<int32_t>(v);
             if (i == j) dgt[i] = static_cast<int32_t>(v);
             for (int sl = 0; sl < ubqp::kSlices; ++sl) {
@@ -689,12 +904,23 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
                 L[sl * plane + static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(d);
                 v = (v - d) / 128;
             }
+            // evaluation image: exact balanced base-128 digits of rint(Q 2^e_w), top digit |d| <= 127
+            __int128 V = scaled_int(q, e_w);
+            for (int sl = 0; sl < limbs; ++sl) {
+                const int r = static_cast<int>(((V % 128) + 128) % 128);
+                const int d = sl == limbs - 1 ? static_cast<int>(V) : (r >= 64 ? r - 128 : r);
+                W[sl * plane + static_cast<size_t>(i) * h->q_ld + j] = static_cast<int8_t>(d);
+                if (j <= i) WL[sl * tplane + static_cast<size_t>(i) * h->n_pad + j] = static_cast<int8_t>(d);
+                if (i == j) wdg[static_cast<size_t>(sl) * h->q_rows + i] = d;
+                V = (V - d) / 128;
+            }
         }
     const int64_t nblk = (k_max + 4095) / 4096 + 1;
     h->k_max = k_max;
     h->k_cap_pad = (k_max + ubqp::kBM - 1) / ubqp::kBM * ubqp::kBM;
     bool ok = cudaMalloc(&h->seed, h->W64 * sizeof(uint64_t)) == cudaSuccess &&
-              cudaMalloc(&h->diag, h->q_rows * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&h->zdiag, h->q_rows * sizeof(int32_t)) == cudaSuccess &&
+              cudaMalloc(&h->wdiag, wdg.size() * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&h->Xb, k_max * h->W64 * sizeof(uint64_t)) == cudaSuccess &&
               cudaMalloc(&h->X8, h->k_cap_pad * h->n_pad) == cudaSuccess &&
               cudaMalloc(&h->f, k_max * sizeof(int64_t)) == cudaSuccess &&
@@ -704,6 +930,8 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
               cudaMalloc(&h->surv, k_max * sizeof(int32_t)) == cudaSuccess &&
               cudaMalloc(&h->blk_count, nblk * sizeof(int32_t)) == cudaSuccess;
     for (int sl = 0; ok && sl < ubqp::kSlices; ++sl) ok = cudaMalloc(&h->Qs[sl], plane) == cudaSuccess;
+    for (int sl = 0; ok && sl < limbs; ++sl)
+        ok = cudaMalloc(&h->Qw[sl], plane) == cudaSuccess && cudaMalloc(&h->QwL[sl], tplane) == cudaSuccess;
     ok = ok && cudaMalloc(&h->Qt, qt.size() * sizeof(int32_t)) == cudaSuccess &&
          cudaMalloc(&h->diagt, dgt.size() * sizeof(int32_t)) == cudaSuccess;
     if (!ok) {
@@ -711,16 +939,28 @@ int ubqp_load_Q_real(ubqp_t h, int32_t n, int dtype, const void *Q, int64_t k_ma
         free_all(*h);
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the real-Q workspace");
     }
-    CK(cudaMemset(h->diag, 0, h->q_rows * sizeof(int32_t)));   // plane gains carry no diagonal (R20)
+    CK(cudaMemset(h->zdiag, 0, h->q_rows * sizeof(int32_t)));   // walk-plane gains carry no diagonal (R20)
+    CK(cudaMemcpy(h->wdiag, wdg.data(), wdg.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->Qt, qt.data(), qt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->diagt, dgt.data(), dgt.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    const int32_t *zd[1] = {h->zdiag};
     for (int sl = 0; sl < ubqp::kSlices; ++sl) {
         CK(cudaMemcpy(h->Qs[sl], L.data() + sl * plane, plane, cudaMemcpyHostToDevice));
-        if (!encode_map(&h->tmap_Qs[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN, h->q_ld) ||
-            !encode_map(&h->tmap_Qs_h[sl], h->Qs[sl], h->n_pad, h->q_rows, ubqp::kBN / 2, h->q_ld)) {
+        int8_t *pl[1] = {h->Qs[sl]};
+        if (!set_operand(h->op_walk[sl], pl, 1, h->q_ld, false, zd, h->n_pad, h->q_rows)) {
             free_all(*h);
             return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
         }
+    }
+    const int32_t *wd[ubqp::kMaxLimbs];
+    for (int sl = 0; sl < limbs; ++sl) {
+        CK(cudaMemcpy(h->Qw[sl], W.data() + sl * plane, plane, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->QwL[sl], WL.data() + sl * tplane, tplane, cudaMemcpyHostToDevice));
+        wd[sl] = h->wdiag + static_cast<size_t>(sl) * h->q_rows;
+    }
+    if (!set_operand(h->op_wide, h->QwL, limbs, h->n_pad, true, wd, h->n_pad, h->q_rows)) {
+        free_all(*h);
+        return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
     }
     CK(cudaMemset(h->X8, 0, h->k_cap_pad * h->n_pad));
     if (!encode_map(&h->tmap_X8, h->X8, h->n_pad, h->k_cap_pad, ubqp::kBM)) {
@@ -736,30 +976,44 @@ int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out) {
     GUARD(h);
     if (!h->real) return fail(h, UBQP_E_STATE, "ubqp: no real-valued Q loaded");
     if (h->k_local < 0) return fail(h, UBQP_E_STATE, "ubqp: no batch to evaluate");
+    static_assert(sizeof(ubqp_stats_real) == 6 * sizeof(int64_t), "ubqp_stats_real layout");
     const int64_t k = h->k_local;
-    if (k > 0) {
-        CK(cudaMemsetAsync(h->fs, 0, ubqp::kSlices * h->k_max * sizeof(int64_t), h->stream));
-        for (int sl = 0; sl < ubqp::kSlices; ++sl) {
-            ubqp::launch_eval_tc(*h, k, false, sl, h->fs + sl * h->k_max);
-            CK_LAUNCH("eval_tc_kernel (plane)");
-        }
+    const bool f_dev = f_out && is_device_ptr(f_out);
+    const bool s_dev = stats_out && is_device_ptr(stats_out);
+    int64_t *st = h->scratch64 + 8;
+    if (k == 0) {
+        const int64_t z[6] = {0, 0, 0, INT64_MIN, 0, static_cast<int64_t>(static_cast<uint32_t>(h->w_exp))};
+        CK(cudaMemcpyAsync(st, z, sizeof z, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    } else {
+        // one launch: every limb plane of the evaluation image, f and int128 stats folded in-kernel
+        ubqp::EvalLaunch L;
+        L.tmX = &h->tmap_X8;
+        L.Xb = h->Xb;
+        L.k = k;
+        L.op = &h->op_wide;
+        L.mode = ubqp::kFoldReal;
+        L.fr = h->freal;
+        L.fr2 = f_dev ? f_out : nullptr;
+        L.stats = st;
+        L.stats2 = s_dev ? reinterpret_cast<int64_t *>(stats_out) : nullptr;
+        L.rank = h->rank;
+        L.world = h->world;
+        L.q_exp = h->w_exp;
+        const int rc = eval_launch(h, L);
+        if (rc) return rc;
     }
-    ubqp::launch_combine_real(*h, k, h->scratch64 + 8);
-    CK_LAUNCH("combine_real_kernel");
     h->freal_valid = true;
     h->gains64_valid = false;
     bool sync = false;
-    if (f_out && k > 0) {
-        const bool dev = is_device_ptr(f_out);
-        CK(cudaMemcpyAsync(f_out, h->freal, k * sizeof(double), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                           h->stream));
-        sync |= !dev;
+    if (f_out && !f_dev && k > 0) {
+        CK(cudaMemcpyAsync(f_out, h->freal, k * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        sync = true;
     }
-    if (stats_out) {
-        const bool dev = is_device_ptr(stats_out);
-        CK(cudaMemcpyAsync(stats_out, h->scratch64 + 8, 4 * sizeof(int64_t),
-                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
-        sync |= !dev;
+    if (stats_out && (!s_dev || k == 0)) {
+        CK(cudaMemcpyAsync(stats_out, st, sizeof(ubqp_stats_real), s_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                           h->stream));
+        sync |= !s_dev;
     }
     if (sync) CK(cudaStreamSynchronize(h->stream));
     return UBQP_OK;
@@ -776,7 +1030,7 @@ int ubqp_screen_real(ubqp_t h, double lambda, double mean, double max_value, int
     volatile double scaled = lambda * diff;
     const double T = mean + scaled;
     if (T_out) *T_out = T;
-    ubqp::launch_screen_real(*h, h->k_local, T, h->scratch64 + 4);
+    CK(ubqp::launch_screen_real(*h, h->k_local, T, h->scratch64 + 4));
     CK_LAUNCH("screen kernels (real)");
     int64_t m = 0;
     CK(cudaMemcpyAsync(&m, h->scratch64 + 4, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
@@ -809,12 +1063,35 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
         case UBQP_Q_STREAM: *value = reinterpret_cast<int64_t>(h->stream); break;
         case UBQP_Q_REAL_EXP: *value = h->real ? h->q_exp : 0; break;
         case UBQP_Q_IS_REAL: *value = h->real ? 1 : 0; break;
+        case UBQP_Q_EVAL_EXP: *value = h->real ? h->w_exp : 0; break;
+        case UBQP_Q_EVAL_LIMBS: *value = h->real ? h->w_limbs : 1; break;
+        case UBQP_Q_NNZ: *value = h->nnz; break;
+        case UBQP_Q_SPARSE_ROWS: *value = h->csr_ptr ? 1 : 0; break;
         default: return UBQP_E_INVALID;
     }
     return UBQP_OK;
 }
 
-}  // extern "C"
+int ubqp_set_option(ubqp_t h, int what, int64_t value) {
+    GUARD(h);
+    switch (what) {
+        case UBQP_OPT_ASCENT:
+            if (value < 0 || value > 2) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_ASCENT must be 0, 1 or 2");
+            h->asc_kernel = static_cast<int>(value);
+            break;
+        case UBQP_OPT_EVAL_PAIR:
+            if (value != 0 && value != 1) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_EVAL_PAIR must be 0 or 1");
+            h->eval_pair = value == 1;
+            break;
+        case UBQP_OPT_EVAL_TRI:
+            if (value != 0 && value != 1) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_EVAL_TRI must be 0 or 1");
+            h->sym_eval = value == 1;
+            break;
+        default:
+            return fail(h, UBQP_E_INVALID, "ubqp: unknown option");
+    }
+    return UBQP_OK;
+}
 
 int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, double *f_out,
                      int64_t *fint_out, int32_t *flips_out, uint64_t *bits_out) {
@@ -834,10 +1111,19 @@ int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flip
                 return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the int64 gains buffer");
             }
         }
-        // Delta~ = Qt_jj + sum_s 128^s 2 (1 - 2x) Y_s: plane gains (zero diagonal) combined exactly
+        // walk image (R20): Delta~ = Qt_jj + sum_s 128^s 2 (1 - 2x) Y_s from the four walk planes
+        // (zero diagonal) and f~28 = sum_s 128^s x^t L_s x, combined exactly
         for (int sl = 0; sl < ubqp::kSlices; ++sl) {
-            ubqp::launch_eval_tc(*h, k, true, sl, h->fs + sl * h->k_max);
-            CK_LAUNCH("eval_tc_kernel (plane gains)");
+            ubqp::EvalLaunch L;
+            L.tmX = &h->tmap_X8;
+            L.Xb = h->Xb;
+            L.k = k;
+            L.op = &h->op_walk[sl];
+            L.emit_gains = true;
+            L.mode = ubqp::kFoldPlane;
+            L.f = h->fs + sl * h->k_max;
+            rc = eval_launch(h, L);
+            if (rc) return rc;
             ubqp::launch_gains_combine(*h, k, sl);
             CK_LAUNCH("gains_combine_kernel");
         }
@@ -849,11 +1135,13 @@ int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flip
     if (m > 0 && !is_device_ptr(slots)) {
         for (int64_t i = 0; i < m; ++i)
             if (slots[i] < 0 || slots[i] >= h->k_local) return fail(h, UBQP_E_INVALID, "ubqp: slot out of range");
-        CK(cudaMemcpyAsync(h->asc_slots, slots, m * sizeof(int32_t), cudaMemcpyHostToDevice, h->stream));
+        const int rc2 = h2d_sync(h, h->asc_slots, slots, m * sizeof(int32_t));
+        if (rc2) return rc2;
         slots_dev = h->asc_slots;
     }
     if (m == 0) return UBQP_OK;
-    // device outputs pass through; host outputs go through scratch (f as int64 bits in asc_f)
+    // device outputs pass through; host outputs go through scratch.  The final bits always land
+    // in device memory: f of each local optimum is re-evaluated on the evaluation image (R22).
     const bool f_dev = f_out && is_device_ptr(f_out);
     const bool i_dev = fint_out && is_device_ptr(fint_out);
     const bool fl_dev = flips_out && is_device_ptr(flips_out);
@@ -862,15 +1150,42 @@ int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flip
     int64_t *fi_d = i_dev ? fint_out : nullptr;
     int64_t *fi_host_tmp = nullptr;
     if (fint_out && !i_dev) {
-        // second scratch: reuse the per-slot stats area of the planes (fs has kSlices * k_max)
+        // second scratch: the per-walk-plane values (fs has kSlices * k_max; fint is already formed)
         fi_d = h->fs;
         fi_host_tmp = fint_out;
     }
     int32_t *fl_d = fl_dev ? flips_out : h->asc_flips;
-    uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
-    if (ubqp::launch_ascend_real(*h, slots_dev, m, max_flips, fr_d, fi_d, fl_d, b_d))
+    uint64_t *b_d = b_dev ? bits_out : h->asc_bits;
+    if (ubqp::launch_ascend_real(*h, slots_dev, m, max_flips, nullptr, fi_d, fl_d, b_d))
         return fail(h, UBQP_E_RANGE, "ubqp: n outside the real ascent kernel range");
     CK_LAUNCH("ascend_real_kernel");
+    if (fr_d) {
+        if (!h->X8r) {
+            if (cudaMalloc(&h->X8r, ubqp::kReevalRows * h->n_pad) != cudaSuccess) {
+                cudaGetLastError();
+                h->X8r = nullptr;
+                return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the re-evaluation workspace");
+            }
+            if (!encode_map(&h->tmap_X8r, h->X8r, h->n_pad, ubqp::kReevalRows, ubqp::kBM))
+                return fail(h, UBQP_E_CUDA, "ubqp: cuTensorMapEncodeTiled failed");
+        }
+        for (int64_t c0 = 0; c0 < m; c0 += ubqp::kReevalRows) {
+            const int64_t cm = std::min<int64_t>(ubqp::kReevalRows, m - c0);
+            ubqp::launch_expand_to(*h, b_d + c0 * h->W64, cm, h->X8r);
+            CK_LAUNCH("expand_kernel (re-evaluation)");
+            ubqp::EvalLaunch L;
+            L.tmX = &h->tmap_X8r;
+            L.Xb = b_d + c0 * h->W64;
+            L.k = cm;
+            L.op = &h->op_wide;
+            L.mode = ubqp::kFoldReal;
+            L.fr = fr_d + c0;
+            L.stats = h->scratch64 + 16;   // not reported
+            L.q_exp = h->w_exp;
+            rc = eval_launch(h, L);
+            if (rc) return rc;
+        }
+    }
     bool sync = false;
     if (f_out && !f_dev) { CK(cudaMemcpyAsync(f_out, fr_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
     if (fi_host_tmp) { CK(cudaMemcpyAsync(fi_host_tmp, fi_d, m * 8, cudaMemcpyDeviceToHost, h->stream)); sync = true; }
@@ -886,3 +1201,5 @@ int ubqp_ascend_real(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flip
     }
     return UBQP_OK;
 }
+
+}  // extern "C"

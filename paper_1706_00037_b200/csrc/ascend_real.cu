@@ -21,15 +21,25 @@ namespace {
 constexpr int kRB = 256;                 // threads per solution
 constexpr long long kRPad = LLONG_MIN / 2;   // padding / parked keys: never the maximum
 
+// gains64 (+)= gains << 7 plane (plane 0 starts from the walk diagonal Qt_jj); with the last
+// plane, also f~28 = sum_s 128^s f_s of every row (the walk's starting value)
 __global__ void __launch_bounds__(256) gains_combine_kernel(const int32_t *__restrict__ g32,
                                                             int64_t *__restrict__ g64,
                                                             const int32_t *__restrict__ diagt, int64_t k,
-                                                            int n_pad, int shift, int first) {
+                                                            int n_pad, int shift, int first,
+                                                            const int64_t *__restrict__ fs, int64_t k_max,
+                                                            int64_t *__restrict__ fint) {
     const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (idx >= k * n_pad) return;
     const int j = static_cast<int>(idx % n_pad);
     const int64_t base = first ? static_cast<int64_t>(diagt[j]) : g64[idx];
     g64[idx] = base + (static_cast<int64_t>(g32[idx]) << shift);
+    if (fint && j == 0) {
+        const int64_t row = idx / n_pad;
+        int64_t v = 0;
+        for (int s = kSlices - 1; s >= 0; --s) v = v * 128 + fs[s * k_max + row];
+        fint[row] = v;
+    }
 }
 
 template <int NPT, int MINB>
@@ -160,11 +170,9 @@ void launch_real_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips
     constexpr int kByS = (228 * 1024) / (kSmem + 3 * 1024);
     constexpr int kByR = 65536 / (kRB * (NPT + 40));
     constexpr int kMinB = (kByS < kByR ? kByS : kByR) < 1 ? 1 : (kByS < kByR ? kByS : kByR);
-    static bool attr = false;                 // one opt-in per instantiation (> 48 KB dynamic)
-    if (!attr) {
-        cudaFuncSetAttribute(ascend_real_kernel<NPT, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        attr = true;
-    }
+    // > 48 KB dynamic opt-in: per device context, so set before every launch (cheap) rather
+    // than once per process (a second device would otherwise fail to launch)
+    cudaFuncSetAttribute(ascend_real_kernel<NPT, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     ascend_real_kernel<NPT, kMinB><<<static_cast<unsigned>(m), kRB, kSmem, c.stream>>>(
         slots, max_flips, c.n, c.n_pad, c.qt_ld, c.W64, c.k_local, c.Qt, c.gains64, c.fint, c.Xb, c.q_exp, f_dev,
         fint_dev, flips_dev, bits_dev);
@@ -182,7 +190,8 @@ void launch_gains_combine(Ctx &c, int64_t k, int plane) {
     if (k <= 0) return;
     const int64_t tot = k * c.n_pad;
     gains_combine_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, c.stream>>>(
-        c.gains, c.gains64, c.diagt, k, c.n_pad, 7 * plane, plane == 0 ? 1 : 0);
+        c.gains, c.gains64, c.diagt, k, c.n_pad, 7 * plane, plane == 0 ? 1 : 0, c.fs, c.k_max,
+        plane == kSlices - 1 ? c.fint : nullptr);
     ++c.launches;
 }
 

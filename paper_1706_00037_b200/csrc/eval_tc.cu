@@ -1,18 +1,26 @@
 // eval_tc.cu — K-EVAL: batched xQx on 5th-generation tensor cores.
 //
-// Y = X8 · Q8  (s8 x s8 -> s32, exact), never written to HBM: the accumulator tile lives
-// in TMEM and the epilogue folds it immediately into
+// Y = X8 · B  (s8 x s8 -> s32, exact), never written to HBM: the accumulator tile lives in
+// TMEM and the epilogue folds it immediately into
 //     f_k      = sum_j x_kj Y_kj                         (P:24 eq. (P); Appendix A of SURVEY)
 //     Delta_kj = Q_jj + 2 (1 - 2 x_kj) Y_kj              (P:53 1-flip gains; UBQP_EMIT_GAINS)
-// A = X8 [K x n_pad] K-major; B = Q8 [q_rows x n_pad] row-major, which is the "N x K,
-// K-major" operand because Q = Q^t (row j of Q8 = column j of Q).
+// A = X8 [K x n_pad] K-major; B = an int8 plane of Q [q_rows x n_pad] row-major, which is the
+// "N x K, K-major" operand because Q = Q^t (row j = column j).  One launch may run several
+// planes (the limb planes of a real-valued Q, a4'): f~ = sum_s 128^s x^t L_s x.
 //
-// Persistent warp-specialised kernel, one CTA per SM:
-//   warp 0      : TMA producer (128B-swizzled 128x128 A and 256x128 B boxes, kStages ring)
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=256, K=32)
-//   warps 2..5  : epilogue (tcgen05.ld 32x32b -> f partial / gains), TMEM double-buffered
-// Tiles are ordered n-fastest so the ~5 X bands in flight are shared through L2 by all
-// N tiles and Q (49 MB at n = 7000) stays L2-resident.
+// Persistent warp-specialised kernels, one CTA (or CTA pair) per SM:
+//   warp 0      : TMA producer (128B-swizzled boxes, smem ring)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  : epilogue (tcgen05.ld 32x32b, thread = row), TMEM double-buffered
+// Work item = (plane, M tile, N tile, K split), plane outermost (each plane stays
+// L2-resident for its pass), N fastest (the X band in flight is shared through L2).
+//
+// f and the screening statistics are folded in-kernel (north_star: "the mean/max screening
+// reduction fused into the epilogue"): every item stores its int32 row partials, and the
+// last item to arrive for a 128-row group (an atomic counter per group) sums them into f,
+// reduces the group's {sum f, max_key}; the last group to finish reduces all groups into the
+// stats.  Counters reset themselves, so one launch per evaluation, no memset, no stats kernel.
+#include <algorithm>
 #include <climits>
 
 #include "ubqp_internal.cuh"
@@ -25,8 +33,276 @@ constexpr uint32_t kABytes = kBM * kBK;             // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK;             // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
 constexpr uint32_t kTmemCols = 2 * kBN;             // two 128 x 256 s32 accumulators
-constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 256;
+constexpr size_t kSmemBytes = static_cast<size_t>(kStages) * kStageBytes + 1024 + 512;
 constexpr uint32_t kIdesc = dev::idesc_i8(kBM, kBN);
+
+constexpr int kPairStages = 6;
+constexpr uint32_t kPairStageBytes = 2 * kABytes;                    // 16 KB A + 16 KB B
+constexpr size_t kPairSmemBytes = static_cast<size_t>(kPairStages) * kPairStageBytes + 1024 + 512;
+constexpr uint32_t kIdescPair = dev::idesc_i8(2 * kBM, kBN);
+
+// Kernel arguments (one __grid_constant__ block: the B tensor maps of every plane included).
+struct EvalParams {
+    CUtensorMap tmX;                      // A = X8
+    CUtensorMap tmB[kMaxPlanes];          // B per plane (256-row boxes single-CTA, 128-row pair)
+    const int32_t *diag[kMaxPlanes];      // per-plane diagonal (SYM term, gains)
+    int planes;
+    int n_pad, W64, num_n_tiles, num_k_blocks, ksplit;
+    int64_t K, mn_tiles, num_items;
+    const uint64_t *Xb;
+    int32_t *gains;                       // EMIT_GAINS target [K][n_pad] (single plane launches)
+    int emit_gains;
+    // fold
+    int32_t *part;                        // [planes][num_n_tiles][ksplit][part_ld] int32 row partials
+    int64_t part_ld;
+    unsigned *grp_cnt;                    // [num_groups] arrival counters, then [num_groups]: done
+    int items_per_group;
+    int64_t num_groups;
+    int64_t *grp_res;                     // [num_groups][4]
+    int mode;                             // kFoldInt / kFoldPlane / kFoldReal
+    int64_t *f, *f2;                      // int f (kFoldInt, kFoldPlane); f2 optional second copy
+    double *fr, *fr2;                     // real f (kFoldReal)
+    int64_t *stats, *stats2;              // int: {sum, K, max_key, 0}; real: ubqp_stats_real words
+    int rank, world, q_exp;
+};
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __forceinline__ int kbs_of(int nt, int num_k_blocks, bool sym) {
+    return sym ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
+}
+
+// int128 helpers (hi signed, lo unsigned)
+constexpr __int128 kI128Min = static_cast<__int128>(static_cast<unsigned __int128>(1) << 127);
+struct I128 {
+    long long hi;
+    unsigned long long lo;
+};
+__device__ __forceinline__ I128 to_i128(__int128 v) {
+    return {static_cast<long long>(v >> 64), static_cast<unsigned long long>(v)};
+}
+__device__ __forceinline__ __int128 from_i128(long long hi, unsigned long long lo) {
+    return (static_cast<__int128>(hi) << 64) | static_cast<__int128>(lo);
+}
+// correctly rounded int128 -> binary64: the top 64 significant bits with a sticky bit in the
+// lsb round to 53 bits exactly as the full value would (cvt.rn.f64.u64 rounds to nearest even)
+__device__ __forceinline__ double i128_to_double(__int128 v) {
+    const bool neg = v < 0;
+    const unsigned __int128 a = neg ? static_cast<unsigned __int128>(-(v + 1)) + 1u : static_cast<unsigned __int128>(v);
+    const unsigned long long hi = static_cast<unsigned long long>(a >> 64);
+    double d;
+    if (hi == 0) {
+        d = __ull2double_rn(static_cast<unsigned long long>(a));
+    } else {
+        const int sh = 64 - __clzll(static_cast<long long>(hi));
+        unsigned long long top = static_cast<unsigned long long>(a >> sh);
+        const unsigned __int128 low = a & ((static_cast<unsigned __int128>(1) << sh) - 1u);
+        if (low != 0) top |= 1ull;
+        d = ldexp(__ull2double_rn(top), sh);
+    }
+    return neg ? -d : d;
+}
+
+// ---------------------------------------------------------------- fold (last arriver per group)
+// Called by the 128 epilogue threads of a CTA (t = row in group) after each stored its
+// partial of one work item for rows [128 group, 128 group + 128).
+template <bool SYM>
+__device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, int t, uint32_t *s_flag,
+                                          long long *s_red) {
+    epi_bar();                                         // the 128 partials of this item are stored
+    if (t == 0) {
+        __threadfence();
+        const unsigned old = atomicAdd(&p.grp_cnt[group], 1u);
+        s_flag[0] = old + 1u == static_cast<unsigned>(p.items_per_group) ? 1u : 0u;
+    }
+    epi_bar();
+    if (!s_flag[0]) return;
+    __threadfence();
+    const int64_t row = group * 128 + t;
+    const bool ok = row < p.K;
+    // sum the partials of every (non-empty) item of this group, plane by plane
+    __int128 acc = 0;
+    long long fsum = 0;
+    for (int pl = p.planes - 1; pl >= 0; --pl) {
+        long long s = 0;
+        for (int nt = 0; nt < p.num_n_tiles; ++nt) {
+            const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
+            for (int ks = 0; ks < p.ksplit; ++ks) {
+                if ((ks + 1) * kbs / p.ksplit == ks * kbs / p.ksplit) continue;   // empty item
+                const int64_t si = (static_cast<int64_t>(pl) * p.num_n_tiles + nt) * p.ksplit + ks;
+                s += __ldcg(p.part + si * p.part_ld + row);
+            }
+        }
+        acc = acc * 128 + s;
+        fsum = s;
+    }
+    if (t == 0) p.grp_cnt[group] = 0u;                 // self-reset for the next launch
+    if (p.mode == kFoldPlane) {
+        if (ok) p.f[row] = fsum;
+        return;
+    }
+    // group result: int -> {sum f, max_key}; real -> {sum f~ (int128), max f~ (int128)}
+    const int lane = t & 31, w = t >> 5;
+    if (p.mode == kFoldInt) {
+        long long key = -1, sm = 0;
+        if (ok) {
+            p.f[row] = fsum;
+            if (p.f2) p.f2[row] = fsum;
+            const long long g = static_cast<long long>(p.rank) + row * p.world;
+            key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
+                                         static_cast<unsigned long long>((1ll << 22) - 1 - g));
+            sm = fsum;
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+        }
+        if (lane == 0) {
+            s_red[2 * w] = sm;
+            s_red[2 * w + 1] = key;
+        }
+        epi_bar();
+        if (t == 0) {
+            long long S = 0, M = -1;
+            for (int i = 0; i < 4; ++i) {
+                S += s_red[2 * i];
+                M = max(M, s_red[2 * i + 1]);
+            }
+            p.grp_res[4 * group + 0] = S;
+            p.grp_res[4 * group + 1] = M;
+        }
+    } else {   // kFoldReal
+        __int128 sm = 0, mx = 0;
+        bool have = false;
+        if (ok) {
+            const double fr = ldexp(i128_to_double(acc), -p.q_exp);
+            p.fr[row] = fr;
+            if (p.fr2) p.fr2[row] = fr;
+            sm = acc;
+            mx = acc;
+            have = true;
+        }
+        // warp reduce: sum with carries, max (invalid rows carry have = false)
+        for (int o = 16; o > 0; o >>= 1) {
+            const I128 a = to_i128(sm), b = to_i128(mx);
+            const long long sh = __shfl_xor_sync(0xffffffffu, a.hi, o);
+            const unsigned long long sl = __shfl_xor_sync(0xffffffffu, a.lo, o);
+            const long long mh = __shfl_xor_sync(0xffffffffu, b.hi, o);
+            const unsigned long long ml = __shfl_xor_sync(0xffffffffu, b.lo, o);
+            const int oh = __shfl_xor_sync(0xffffffffu, have ? 1 : 0, o);
+            sm += from_i128(sh, sl);
+            const __int128 om = from_i128(mh, ml);
+            if (oh && (!have || om > mx)) mx = om;
+            have = have || oh;
+        }
+        if (lane == 0) {
+            const I128 a = to_i128(sm), b = to_i128(mx);
+            s_red[5 * w + 0] = a.hi;
+            s_red[5 * w + 1] = static_cast<long long>(a.lo);
+            s_red[5 * w + 2] = b.hi;
+            s_red[5 * w + 3] = static_cast<long long>(b.lo);
+            s_red[5 * w + 4] = have ? 1 : 0;
+        }
+        epi_bar();
+        if (t == 0) {
+            __int128 S = 0, M = 0;
+            bool H = false;
+            for (int i = 0; i < 4; ++i) {
+                S += from_i128(s_red[5 * i], static_cast<unsigned long long>(s_red[5 * i + 1]));
+                if (s_red[5 * i + 4]) {
+                    const __int128 m2 = from_i128(s_red[5 * i + 2], static_cast<unsigned long long>(s_red[5 * i + 3]));
+                    if (!H || m2 > M) M = m2;
+                    H = true;
+                }
+            }
+            if (!H) M = kI128Min;                              // no solution in this group
+            const I128 a = to_i128(S), b = to_i128(M);
+            p.grp_res[4 * group + 0] = a.hi;
+            p.grp_res[4 * group + 1] = static_cast<long long>(a.lo);
+            p.grp_res[4 * group + 2] = b.hi;
+            p.grp_res[4 * group + 3] = static_cast<long long>(b.lo);
+        }
+    }
+    // last group overall folds every group's result into the statistics
+    if (t == 0) {
+        __threadfence();
+        unsigned *done = p.grp_cnt + p.num_groups;
+        const unsigned old = atomicAdd(done, 1u);
+        s_flag[0] = old + 1u == static_cast<unsigned>(p.num_groups) ? 1u : 0u;
+    }
+    epi_bar();
+    if (!s_flag[0]) return;
+    __threadfence();
+    if (p.mode == kFoldInt) {
+        long long S = 0, M = -1;
+        for (int64_t g = t; g < p.num_groups; g += 128) {
+            S += __ldcg(p.grp_res + 4 * g);
+            M = max(M, static_cast<long long>(__ldcg(p.grp_res + 4 * g + 1)));
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            S += __shfl_xor_sync(0xffffffffu, S, o);
+            M = max(M, __shfl_xor_sync(0xffffffffu, M, o));
+        }
+        epi_bar();
+        if (lane == 0) {
+            s_red[2 * w] = S;
+            s_red[2 * w + 1] = M;
+        }
+        epi_bar();
+        if (t == 0) {
+            long long SS = 0, MM = -1;
+            for (int i = 0; i < 4; ++i) {
+                SS += s_red[2 * i];
+                MM = max(MM, s_red[2 * i + 1]);
+            }
+            const long long out[4] = {SS, static_cast<long long>(p.K), MM, 0};
+            for (int i = 0; i < 4; ++i) {
+                p.stats[i] = out[i];
+                if (p.stats2) p.stats2[i] = out[i];
+            }
+            p.grp_cnt[p.num_groups] = 0u;
+        }
+    } else {
+        __int128 S = 0, M = 0;
+        bool H = false;
+        for (int64_t g = t; g < p.num_groups; g += 128) {
+            S += from_i128(__ldcg(p.grp_res + 4 * g), static_cast<unsigned long long>(__ldcg(p.grp_res + 4 * g + 1)));
+            const __int128 m2 =
+                from_i128(__ldcg(p.grp_res + 4 * g + 2), static_cast<unsigned long long>(__ldcg(p.grp_res + 4 * g + 3)));
+            if (!H || m2 > M) M = m2;
+            H = true;
+        }
+        epi_bar();
+        // 128 partial results through shared memory (5 words each), thread 0 combines
+        {
+            const I128 a = to_i128(S), b = to_i128(M);
+            s_red[5 * t + 0] = a.hi;
+            s_red[5 * t + 1] = static_cast<long long>(a.lo);
+            s_red[5 * t + 2] = b.hi;
+            s_red[5 * t + 3] = static_cast<long long>(b.lo);
+            s_red[5 * t + 4] = H ? 1 : 0;
+        }
+        epi_bar();
+        if (t == 0) {
+            __int128 SS = 0, MM = kI128Min;
+            for (int i = 0; i < 128; ++i) {
+                SS += from_i128(s_red[5 * i], static_cast<unsigned long long>(s_red[5 * i + 1]));
+                if (s_red[5 * i + 4]) {
+                    const __int128 m2 = from_i128(s_red[5 * i + 2], static_cast<unsigned long long>(s_red[5 * i + 3]));
+                    if (m2 > MM) MM = m2;
+                }
+            }
+            const I128 a = to_i128(SS), b = to_i128(MM);
+            const long long out[6] = {a.hi, static_cast<long long>(a.lo), static_cast<long long>(p.K), b.hi,
+                                      static_cast<long long>(b.lo), static_cast<long long>(static_cast<unsigned>(p.q_exp))};
+            for (int i = 0; i < 6; ++i) {
+                p.stats[i] = out[i];
+                if (p.stats2) p.stats2[i] = out[i];
+            }
+            p.grp_cnt[p.num_groups] = 0u;
+        }
+    }
+}
 
 // Epilogue of one 128-row x 256-column accumulator (thread = row): drains TMEM 32 columns at a
 // time and folds  f_k += sum_j x_kj Y_kj  (or, triangular: x_kj (2 Y_kj - Q_jj), the Q_jj term
@@ -85,15 +361,33 @@ __device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bo
     return partial;
 }
 
-// SYM (f only, NEXT-1 of SURVEY §8(f)): B = the lower triangle of Q (row j keeps Q_ji, i <= j),
-// so tile column block J needs only K blocks covering rows i < 256(J+1): ~(n+256)/(2n) of the
-// MMAs.  f = sum_j x_j (2 Y^U_j - Q_jj) with Y^U_j = sum_{i<=j} x_i Q_ij  (Q = Q^t).
+// Work item -> (plane, M tile, N tile, K range).  f is linear in Y, so the partial row-dots
+// of K splits add up in the fold; the -Q_jj term of SYM goes with the split owning kb 0.
+struct Item {
+    int plane, mt, nt, ks, kb0, kb1;
+};
 template <bool SYM>
-__global__ void __launch_bounds__(kThreads, 1)
-eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQ,
-               int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
-               const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
-               int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains) {
+__device__ __forceinline__ Item decode_item(const EvalParams &p, int64_t item) {
+    Item it;
+    const int64_t per_plane = p.mn_tiles * p.ksplit;
+    it.plane = static_cast<int>(item / per_plane);
+    const int64_t r = item - static_cast<int64_t>(it.plane) * per_plane;
+    const int64_t mn = r / p.ksplit;
+    it.ks = static_cast<int>(r - mn * p.ksplit);
+    it.mt = static_cast<int>(mn / p.num_n_tiles);
+    it.nt = static_cast<int>(mn - static_cast<int64_t>(it.mt) * p.num_n_tiles);
+    const int kbs = kbs_of(it.nt, p.num_k_blocks, SYM);
+    it.kb0 = it.ks * kbs / p.ksplit;
+    it.kb1 = (it.ks + 1) * kbs / p.ksplit;
+    return it;
+}
+__device__ __forceinline__ int64_t split_index(const EvalParams &p, const Item &it) {
+    return (static_cast<int64_t>(it.plane) * p.num_n_tiles + it.nt) * p.ksplit + it.ks;
+}
+
+// ---------------------------------------------------------------- single-CTA kernel (M = 128)
+template <bool SYM>
+__global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_constant__ EvalParams p) {
     using namespace dev;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -105,6 +399,8 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     uint64_t *tfull = empty + kStages;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint32_t *s_flag = tmem_slot + 1;
+    __shared__ long long s_red[5 * 128];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -119,8 +415,7 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             mbar_init(&tempty[a], 128);
         }
         fence_mbar_init();
-        tma_prefetch(&tmX);
-        tma_prefetch(&tmQ);
+        tma_prefetch(&p.tmX);
     }
     if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
     tc_fence_before();
@@ -135,16 +430,13 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             const uint64_t pol_x = policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                const int m0 = static_cast<int>(tile / num_n_tiles) * kBM;
-                const int nt = static_cast<int>(tile % num_n_tiles);
-                const int n0 = nt * kBN;
-                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
-                for (int kb = 0; kb < kbs; ++kb) {
+            for (int64_t item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+                const Item it = decode_item<SYM>(p, item);
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     mbar_arrive_expect_tx(&full[stage], kStageBytes);
-                    tma_load_2d(sA + stage * kABytes, &tmX, kb * kBK, m0, &full[stage], pol_x);
-                    tma_load_2d(sB + stage * kBBytes, &tmQ, kb * kBK, n0, &full[stage], pol_q);
+                    tma_load_2d(sA + stage * kABytes, &p.tmX, kb * kBK, it.mt * kBM, &full[stage], pol_x);
+                    tma_load_2d(sB + stage * kBBytes, &p.tmB[it.plane], kb * kBK, it.nt * kBN, &full[stage], pol_q);
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
                 }
             }
@@ -156,13 +448,13 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int64_t item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+                const Item it = decode_item<SYM>(p, item);
+                if (it.kb0 == it.kb1) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1u);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
-                const int nt = static_cast<int>(tile % num_n_tiles);
-                const int kbs = SYM ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
-                for (int kb = 0; kb < kbs; ++kb) {
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
@@ -170,8 +462,7 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k) {
                         // +32 bytes along K inside the 128B swizzle atom = +2 in the >>4 field
-                        mma_i8(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdesc,
-                               (kb | k) != 0 ? 1u : 0u);
+                        mma_i8(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdesc, (kb != it.kb0 || k != 0) ? 1u : 0u);
                     }
                     mma_commit(&empty[stage]);   // frees the smem slot when these MMAs retire
                     if (++stage == kStages) { stage = 0; phase ^= 1u; }
@@ -184,23 +475,23 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
         // ---------------- epilogue: warp w may read TMEM lanes 32*(w%4) .. +31
         const int quarter = warp & 3;
         const int row_in_tile = quarter * 32 + lane;
+        const int t = threadIdx.x - 64;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int64_t m0 = (tile / num_n_tiles) * kBM;
-            const int n0 = static_cast<int>(tile % num_n_tiles) * kBN;
-            const int64_t row = m0 + row_in_tile;
-            const bool row_ok = row < K;
+        for (int64_t item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+            const Item it = decode_item<SYM>(p, item);
+            if (it.kb0 == it.kb1) continue;
+            const int64_t row = static_cast<int64_t>(it.mt) * kBM + row_in_tile;
+            const bool row_ok = row < p.K;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int32_t partial = epilogue_tile<SYM>(
-                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN),
-                row, row_ok, n0, W64, n_pad, Xb, diag, gains, emit_gains, true);
+                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
+                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
-            if (row_ok)
-                atomicAdd(reinterpret_cast<unsigned long long *>(f + row),
-                          static_cast<unsigned long long>(static_cast<int64_t>(partial)));
+            p.part[split_index(p, it) * p.part_ld + row] = partial;
+            group_arrive<SYM>(p, it.mt, t, s_flag, s_red);
             if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
     }
@@ -212,41 +503,15 @@ eval_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ 
     }
 }
 
-// ---------------------------------------------------------------- CTA-pair variant
+// ---------------------------------------------------------------- CTA-pair kernel (M = 256)
 // cta_group::2: a cluster of two CTAs on one TPC computes a 256 x 256 tile with M = 256 MMAs
-// issued by the leader; each CTA stages its 128 rows of X and its 128 rows of Q per K block
+// issued by the leader; each CTA stages its 128 rows of X and its 128 rows of B per K block
 // (32 KB per stage instead of 48 KB), so the shared-memory and L2 traffic per MAC halves for
-// B.  Accumulators: each CTA's TMEM holds its 128 rows x 256 columns (two buffers).
-constexpr int kPairStages = 6;
-constexpr uint32_t kPairStageBytes = 2 * kABytes;                    // 16 KB A + 16 KB B
-constexpr size_t kPairSmemBytes = static_cast<size_t>(kPairStages) * kPairStageBytes + 1024 + 256;
-constexpr uint32_t kIdescPair = dev::idesc_i8(2 * kBM, kBN);
-
-// Work item = (M tile of 256 rows, N tile of 256 columns, K split).  f-only launches with
-// fewer tiles than CTA pairs split K (f is linear in Y, so the partial row-dots of the splits
-// add up in the int64 atomics; the -Q_jj term of SYM goes with split 0).
-struct PairTile {
-    int mt, nt, kb0, kb1;
-};
-template <bool SYM>
-__device__ __forceinline__ PairTile pair_tile(int64_t tile, int num_n_tiles, int num_k_blocks, int ksplit) {
-    PairTile t;
-    const int64_t mn = tile / ksplit;
-    const int ks = static_cast<int>(tile - mn * ksplit);
-    t.mt = static_cast<int>(mn / num_n_tiles);
-    t.nt = static_cast<int>(mn - static_cast<int64_t>(t.mt) * num_n_tiles);
-    const int kbs = SYM ? min(num_k_blocks, (t.nt + 1) * (kBN / kBK)) : num_k_blocks;
-    t.kb0 = ks * kbs / ksplit;
-    t.kb1 = (ks + 1) * kbs / ksplit;
-    return t;
-}
-
+// B.  Accumulators: each CTA's TMEM holds its 128 rows x 256 columns (two buffers).  Each
+// CTA's epilogue folds its own 128-row group.
 template <bool SYM>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmQh,
-                    int64_t K, int n_pad, int W64, int num_n_tiles, int num_k_blocks, int64_t num_tiles,
-                    const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
-                    int64_t *__restrict__ f, int32_t *__restrict__ gains, int emit_gains, int ksplit) {
+eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     using namespace dev;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -258,6 +523,8 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     uint64_t *tfull = empty + kPairStages;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint32_t *s_flag = tmem_slot + 1;
+    __shared__ long long s_red[5 * 128];
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -275,8 +542,7 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             mbar_init(&tempty[a], 8);         // 4 epilogue warps x 2 CTAs (leader's copy is used)
         }
         fence_mbar_init();
-        tma_prefetch(&tmX);
-        tma_prefetch(&tmQh);
+        tma_prefetch(&p.tmX);
     }
     if (warp == 1) tmem_alloc_cg2(tmem_slot, kTmemCols);
     tc_fence_before();
@@ -291,17 +557,16 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             const uint64_t pol_x = policy_evict_normal();
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
-                const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
-                if (pt.kb0 == pt.kb1) continue;
-                const int m0 = pt.mt * (2 * kBM) + static_cast<int>(rank) * kBM;
-                const int n0 = pt.nt * kBN + static_cast<int>(rank) * (kBN / 2);
-                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
+            for (int64_t item = cid; item < p.num_items; item += ncl) {
+                const Item it = decode_item<SYM>(p, item);
+                const int m0 = it.mt * (2 * kBM) + static_cast<int>(rank) * kBM;
+                const int n0 = it.nt * kBN + static_cast<int>(rank) * (kBN / 2);
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1u);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kPairStageBytes);
                     const uint32_t fb = mapa_u32(&full[stage], 0);
-                    tma_load_2d_cg2(sA + stage * kABytes, &tmX, kb * kBK, m0, fb, pol_x);
-                    tma_load_2d_cg2(sB + stage * kABytes, &tmQh, kb * kBK, n0, fb, pol_q);
+                    tma_load_2d_cg2(sA + stage * kABytes, &p.tmX, kb * kBK, m0, fb, pol_x);
+                    tma_load_2d_cg2(sB + stage * kABytes, &p.tmB[it.plane], kb * kBK, n0, fb, pol_q);
                     if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
                 }
             }
@@ -313,13 +578,13 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
-                const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
-                if (pt.kb0 == pt.kb1) continue;
+            for (int64_t item = cid; item < p.num_items; item += ncl) {
+                const Item it = decode_item<SYM>(p, item);
+                if (it.kb0 == it.kb1) continue;
                 mbar_wait(&tempty[acc], acc_phase ^ 1u);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * kBN);
-                for (int kb = pt.kb0; kb < pt.kb1; ++kb) {
+                for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
@@ -327,7 +592,7 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
 #pragma unroll
                     for (int k = 0; k < kBK / kUmmaK; ++k)
                         mma_i8_cg2(d_tmem, adesc + 2u * k, bdesc + 2u * k, kIdescPair,
-                                   (kb != pt.kb0 || k != 0) ? 1u : 0u);
+                                   (kb != it.kb0 || k != 0) ? 1u : 0u);
                     mma_commit_pair(&empty[stage]);
                     if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
                 }
@@ -339,29 +604,27 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
         // ---------------- epilogue (both CTAs: their own 128 rows)
         const int quarter = warp & 3;
         const int row_in_tile = quarter * 32 + lane;
+        const int t = threadIdx.x - 64;
         const uint32_t tempty_leader0 = mapa_u32(&tempty[0], 0);
         const uint32_t tempty_leader1 = mapa_u32(&tempty[1], 0);
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t tile = cid; tile < num_tiles; tile += ncl) {
-            const PairTile pt = pair_tile<SYM>(tile, num_n_tiles, num_k_blocks, ksplit);
-            if (pt.kb0 == pt.kb1) continue;
-            const bool with_diag = pt.kb0 == 0;
-            const int64_t m0 = static_cast<int64_t>(pt.mt) * (2 * kBM) + rank * kBM;
-            const int n0 = pt.nt * kBN;
-            const int64_t row = m0 + row_in_tile;
-            const bool row_ok = row < K;
+        for (int64_t item = cid; item < p.num_items; item += ncl) {
+            const Item it = decode_item<SYM>(p, item);
+            if (it.kb0 == it.kb1) continue;
+            const int64_t group = static_cast<int64_t>(it.mt) * 2 + rank;
+            const int64_t row = group * kBM + row_in_tile;
+            const bool row_ok = row < p.K;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int32_t partial = epilogue_tile<SYM>(
-                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN),
-                row, row_ok, n0, W64, n_pad, Xb, diag, gains, emit_gains, with_diag);
+                tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
+                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
-            if (row_ok)
-                atomicAdd(reinterpret_cast<unsigned long long *>(f + row),
-                          static_cast<unsigned long long>(static_cast<int64_t>(partial)));
+            p.part[split_index(p, it) * p.part_ld + row] = partial;
+            group_arrive<SYM>(p, group, t, s_flag, s_red);
             if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
     }
@@ -374,166 +637,104 @@ eval_tc_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_consta
     }
 }
 
-
-// ---------------------------------------------------------------- batch statistics
-__global__ void __launch_bounds__(1024) stats_kernel(const int64_t *__restrict__ f, int64_t K,
-                                                     int rank, int world,
-                                                     int64_t *__restrict__ out) {
-    __shared__ int64_t s_sum[32], s_key[32];
-    int64_t sum = 0, key = -1;
-    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-        const int64_t v = f[i];
-        sum += v;
-        const int64_t g = static_cast<int64_t>(rank) + i * world;
-        const int64_t k = static_cast<int64_t>(
-            (static_cast<uint64_t>(v + (1ll << 40)) << 22) |
-            static_cast<uint64_t>((1ll << 22) - 1 - g));
-        key = k > key ? k : key;
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        sum += __shfl_xor_sync(0xffffffffu, sum, o);
-        const int64_t other = __shfl_xor_sync(0xffffffffu, key, o);
-        key = other > key ? other : key;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        s_sum[threadIdx.x >> 5] = sum;
-        s_key[threadIdx.x >> 5] = key;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int64_t S = 0, M = -1;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-            S += s_sum[w];
-            M = s_key[w] > M ? s_key[w] : M;
-        }
-        out[0] = S;
-        out[1] = K;
-        out[2] = M;
-        out[3] = 0;
-    }
-}
-
-
 }  // namespace
 
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane, int64_t *f_out, bool sym) {
-    const CUtensorMap *tmap_q = plane >= 0 ? &c.tmap_Qs[plane] : nullptr;
-    if (k <= 0) return;
-    if (!c.eval_attr_set) {   // per handle (= per device): the attribute is per device context
-        cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemBytes));
-        cudaFuncSetAttribute(eval_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(kSmemBytes));
-        c.eval_attr_set = true;
+// Shapes of a launch (host): items, groups and the partial buffer it needs.
+EvalShape eval_shape(const Ctx &c, int64_t k, int planes, bool emit_gains, bool sym) {
+    EvalShape s;
+    s.pair = c.eval_pair;
+    s.num_n_tiles = (c.n + kBN - 1) / kBN;
+    s.num_k_blocks = c.n_pad / kBK;
+    const int rows = s.pair ? 2 * kBM : kBM;
+    s.num_m_tiles = (k + rows - 1) / rows;
+    s.mn_tiles = s.num_m_tiles * s.num_n_tiles;
+    s.ksplit = 1;
+    // f-only launches too small to fill the pairs twice split K (<= 8 ways)
+    if (s.pair && !emit_gains)
+        while (s.ksplit < 8 && s.mn_tiles * planes * s.ksplit < c.num_sms && s.num_k_blocks >= 4 * s.ksplit)
+            s.ksplit *= 2;
+    s.num_items = s.mn_tiles * planes * s.ksplit;
+    int nonempty = 0;
+    for (int nt = 0; nt < s.num_n_tiles; ++nt) {
+        const int kbs = sym ? std::min(s.num_k_blocks, (nt + 1) * (kBN / kBK)) : s.num_k_blocks;
+        for (int ks = 0; ks < s.ksplit; ++ks)
+            if ((ks + 1) * kbs / s.ksplit != ks * kbs / s.ksplit) ++nonempty;
     }
-    const int num_n_tiles = (c.n + kBN - 1) / kBN;
-    const int num_k_blocks = c.n_pad / kBK;
-    const bool use_sym = sym && !emit_gains;
-    if (c.eval_pair) {
-        if (!c.eval_pair_attr_set) {
+    s.items_per_group = planes * nonempty;
+    s.num_groups = s.num_m_tiles * (s.pair ? 2 : 1);
+    s.part_ld = s.num_groups * kBM;
+    s.part_elems = static_cast<int64_t>(planes) * s.num_n_tiles * s.ksplit * s.part_ld;
+    return s;
+}
+
+int launch_eval(Ctx &c, const EvalLaunch &L) {
+    if (L.k <= 0) return 0;
+    const bool sym = L.op->tri && !L.emit_gains;
+    const EvalShape s = eval_shape(c, L.k, L.op->planes, L.emit_gains, sym);
+    if (s.part_elems > c.part_cap || s.num_groups + 1 > c.grp_cap) return 1;   // caller sizes first
+    EvalParams p{};
+    p.tmX = *L.tmX;
+    for (int i = 0; i < L.op->planes; ++i) {
+        p.tmB[i] = s.pair ? L.op->half[i] : L.op->full[i];
+        p.diag[i] = L.op->diag[i];
+    }
+    p.planes = L.op->planes;
+    p.n_pad = c.n_pad;
+    p.W64 = c.W64;
+    p.num_n_tiles = s.num_n_tiles;
+    p.num_k_blocks = s.num_k_blocks;
+    p.ksplit = s.ksplit;
+    p.K = L.k;
+    p.mn_tiles = s.mn_tiles;
+    p.num_items = s.num_items;
+    p.Xb = L.Xb;
+    p.gains = L.emit_gains ? c.gains : nullptr;
+    p.emit_gains = L.emit_gains ? 1 : 0;
+    p.part = c.part;
+    p.part_ld = s.part_ld;
+    p.grp_cnt = c.grp_cnt;
+    p.items_per_group = s.items_per_group;
+    p.num_groups = s.num_groups;
+    p.grp_res = c.grp_res;
+    p.mode = L.mode;
+    p.f = L.f;
+    p.f2 = L.f2;
+    p.fr = L.fr;
+    p.fr2 = L.fr2;
+    p.stats = L.stats;
+    p.stats2 = L.stats2;
+    p.rank = L.rank;
+    p.world = L.world;
+    p.q_exp = L.q_exp;
+    if (s.pair) {
+        if (!c.eval_pair_attr_set) {   // per handle (= per device): the attribute is per device context
             cudaFuncSetAttribute(eval_tc_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kPairSmemBytes));
             cudaFuncSetAttribute(eval_tc_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(kPairSmemBytes));
             c.eval_pair_attr_set = true;
         }
-        const int64_t mn_tiles = ((k + 2 * kBM - 1) / (2 * kBM)) * num_n_tiles;
-        // f-only launches too small to fill the pairs twice split K (<= 8 ways)
-        int ksplit = 1;
-        if (!emit_gains)
-            while (ksplit < 8 && mn_tiles * ksplit < c.num_sms && num_k_blocks >= 4 * ksplit) ksplit *= 2;
-        const int64_t num_tiles = mn_tiles * ksplit;
-        const int64_t pairs = num_tiles < c.num_sms / 2 ? num_tiles : c.num_sms / 2;
-        const CUtensorMap &tq = use_sym ? c.tmap_Q8L_h : (plane >= 0 ? c.tmap_Qs_h[plane] : c.tmap_Q8_h);
-        if (use_sym)
-            eval_tc_pair_kernel<true><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
-                c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
-                f_out ? f_out : c.f, nullptr, 0, ksplit);
+        const int64_t pairs = s.num_items < c.num_sms / 2 ? s.num_items : c.num_sms / 2;
+        if (sym)
+            eval_tc_pair_kernel<true><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(p);
         else
-            eval_tc_pair_kernel<false><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(
-                c.tmap_X8, tq, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb, c.diag,
-                f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0, ksplit);
-        ++c.launches;
-        return;
-    }
-    const int64_t num_m_tiles = (k + kBM - 1) / kBM;
-    const int64_t num_tiles = num_m_tiles * num_n_tiles;
-    const int grid = static_cast<int>(num_tiles < c.num_sms ? num_tiles : c.num_sms);
-    if (use_sym)
-        eval_tc_kernel<true><<<grid, kThreads, kSmemBytes, c.stream>>>(
-            c.tmap_X8, c.tmap_Q8L, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks, num_tiles, c.Xb,
-            c.diag, f_out ? f_out : c.f, nullptr, 0);
-    else
-        eval_tc_kernel<false><<<grid, kThreads, kSmemBytes, c.stream>>>(
-            c.tmap_X8, tmap_q ? *tmap_q : c.tmap_Q8, k, c.n_pad, c.W64, num_n_tiles, num_k_blocks,
-            num_tiles, c.Xb, c.diag, f_out ? f_out : c.f, emit_gains ? c.gains : nullptr, emit_gains ? 1 : 0);
-    ++c.launches;
-}
-
-// ---------------------------------------------------------------- real-valued Q (a4')
-// f~_k = sum_s 128^s f_s,k (exact int64), f_k = 2^-q_exp f~_k; stats over the integer image:
-// {sum f~ as int128 (hi, lo), count, max f~} so ranks can reduce them exactly.
-__global__ void __launch_bounds__(1024) combine_real_kernel(const int64_t *__restrict__ fs, int64_t k_max,
-                                                            int64_t K, int q_exp,
-                                                            int64_t *__restrict__ fint,
-                                                            double *__restrict__ freal,
-                                                            int64_t *__restrict__ out) {
-    __shared__ unsigned long long s_lo[32];
-    __shared__ long long s_hi[32];
-    __shared__ long long s_max[32];
-    __int128 sum = 0;
-    long long mx = LLONG_MIN;
-    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-        int64_t v = 0;
-#pragma unroll
-        for (int s = kSlices - 1; s >= 0; --s) v = v * 128 + fs[s * k_max + i];
-        fint[i] = v;
-        freal[i] = ldexp(static_cast<double>(v), -q_exp);
-        sum += v;
-        mx = v > mx ? v : mx;
-    }
-    // reduce the int128 sum as (hi, lo) halves with carries
-    unsigned long long lo = static_cast<unsigned long long>(sum);
-    long long hi = static_cast<long long>(sum >> 64);
-    for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long olo = __shfl_xor_sync(0xffffffffu, lo, o);
-        const long long ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-        const unsigned long long nlo = lo + olo;
-        hi = hi + ohi + (nlo < lo ? 1 : 0);
-        lo = nlo;
-        const long long omx = __shfl_xor_sync(0xffffffffu, mx, o);
-        mx = omx > mx ? omx : mx;
-    }
-    if ((threadIdx.x & 31) == 0) {
-        s_lo[threadIdx.x >> 5] = lo;
-        s_hi[threadIdx.x >> 5] = hi;
-        s_max[threadIdx.x >> 5] = mx;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long L = 0;
-        long long H = 0, M = LLONG_MIN;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) {
-            const unsigned long long nl = L + s_lo[w];
-            H = H + s_hi[w] + (nl < L ? 1 : 0);
-            L = nl;
-            M = s_max[w] > M ? s_max[w] : M;
+            eval_tc_pair_kernel<false><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(p);
+    } else {
+        if (!c.eval_attr_set) {
+            cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemBytes));
+            cudaFuncSetAttribute(eval_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(kSmemBytes));
+            c.eval_attr_set = true;
         }
-        out[0] = H;
-        out[1] = static_cast<int64_t>(L);
-        out[2] = K;
-        out[3] = M;
+        const int grid = static_cast<int>(s.num_items < c.num_sms ? s.num_items : c.num_sms);
+        if (sym)
+            eval_tc_kernel<true><<<grid, kThreads, kSmemBytes, c.stream>>>(p);
+        else
+            eval_tc_kernel<false><<<grid, kThreads, kSmemBytes, c.stream>>>(p);
     }
-}
-
-void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev) {
-    combine_real_kernel<<<1, 1024, 0, c.stream>>>(c.fs, c.k_max, k, c.q_exp, c.fint, c.freal, stats_dev);
     ++c.launches;
-}
-
-void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev) {
-    stats_kernel<<<1, 1024, 0, c.stream>>>(c.f, k, c.rank, c.world, stats_dev);
-    ++c.launches;
+    return 0;
 }
 
 }  // namespace ubqp

@@ -121,33 +121,51 @@ __global__ void __launch_bounds__(256) expand_kernel(int64_t k, int n, int W64, 
     store_expanded(X8 + slot * n_pad + 64ll * w, word);
 }
 
-// x_i = [sum_j Q_ij > 0].  One warp per 32 rows (per-plane row sums fit int32: n*127).
-// Real Q: the row sums of the integer image, sum_s 128^s (row sum of plane s), exact in int64.
+// bits -> bytes of arbitrary device rows (the re-evaluation of ascended real-Q solutions)
+__global__ void __launch_bounds__(256) expand_to_kernel(const uint64_t *__restrict__ bits, int64_t k, int n, int W64,
+                                                        int NW, int n_pad, int8_t *__restrict__ X8) {
+    const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (idx >= k * NW) return;
+    const int64_t slot = idx / NW;
+    const int w = static_cast<int>(idx - slot * NW);
+    const uint64_t word = w < W64 ? bits[slot * W64 + w] & tail_mask(n, w) : 0ull;
+    store_expanded(X8 + slot * n_pad + 64ll * w, word);
+}
+
+// x_i = [sum_j Q_ij > 0].  One block per 32-bit output word (rows 32w .. 32w+31), each
+// of its 8 warps sums 4 rows with 16-byte loads; per plane the row sum fits int32 (n * 127),
+// the planes combine exactly in int128 (a real Q's evaluation image, R22: sum_s 128^s rowsum_s).
 struct Planes {
-    const int8_t *p[kSlices];
+    const int8_t *p[kMaxPlanes];
     int count;
 };
 
-__global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, int n, int n_pad, int q_ld, int W64,
+__global__ void __launch_bounds__(256) first_derivative_kernel(Planes planes, int n, int q_ld,
                                                                uint32_t *__restrict__ bits32) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= 2 * W64) return;
-    // each warp owns one 32-bit output word: rows 32*warp .. 32*warp+31
-    uint32_t word = 0;
-    for (int r = 0; r < 32; ++r) {
-        const int i = warp * 32 + r;
-        long long tot = 0;
+    __shared__ uint32_t s_word;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_word = 0;
+    __syncthreads();
+    for (int r = warp; r < 32; r += 8) {
+        const int i = blockIdx.x * 32 + r;
+        if (i >= n) break;
+        __int128 tot = 0;
         for (int pl = planes.count - 1; pl >= 0; --pl) {
+            const int8_t *row = planes.p[pl] + static_cast<int64_t>(i) * q_ld;
             int s = 0;
-            if (i < n)
-                for (int j = lane; j < n_pad; j += 32) s += planes.p[pl][static_cast<int64_t>(i) * q_ld + j];
+            for (int j0 = 16 * lane; j0 < n; j0 += 16 * 32) {   // rows are zero padded past n
+                const int4 v = *reinterpret_cast<const int4 *>(row + j0);
+                const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s = __dp4a(w[q], 0x01010101, s);
+            }
             s = __reduce_add_sync(0xffffffffu, s);
             tot = tot * 128 + s;
         }
-        if (i < n && tot > 0) word |= 1u << r;
+        if (lane == 0 && tot > 0) atomicOr(&s_word, 1u << r);
     }
-    if (lane == 0) bits32[warp] = word;
+    __syncthreads();
+    if (threadIdx.x == 0) bits32[blockIdx.x] = s_word;
 }
 
 inline unsigned blocks_for(int64_t threads) { return static_cast<unsigned>((threads + 255) / 256); }
@@ -180,17 +198,23 @@ void launch_expand(Ctx &c, int64_t k) {
 }
 
 void launch_first_derivative(Ctx &c, uint64_t *bits_dev) {
-    const int warps = 2 * c.W64;   // one warp per 32-bit output word
     Planes pl{};
     if (c.real) {
-        for (int s = 0; s < kSlices; ++s) pl.p[s] = c.Qs[s];
-        pl.count = kSlices;
+        for (int s = 0; s < c.w_limbs; ++s) pl.p[s] = c.Qw[s];
+        pl.count = c.w_limbs;
     } else {
         pl.p[0] = c.Q8;
         pl.count = 1;
     }
-    first_derivative_kernel<<<(warps * 32 + 255) / 256, 256, 0, c.stream>>>(
-        pl, c.n, c.n_pad, c.q_ld, c.W64, reinterpret_cast<uint32_t *>(bits_dev));
+    // one block per 32-bit word of the W64 output words (2 W64 words, the last may be padding)
+    first_derivative_kernel<<<2 * c.W64, 256, 0, c.stream>>>(pl, c.n, c.q_ld, reinterpret_cast<uint32_t *>(bits_dev));
+    ++c.launches;
+}
+
+void launch_expand_to(Ctx &c, const uint64_t *bits, int64_t k, int8_t *X8dst) {
+    if (k <= 0) return;
+    const int NW = c.n_pad / 64;
+    expand_to_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(bits, k, c.n, c.W64, NW, c.n_pad, X8dst);
     ++c.launches;
 }
 

@@ -72,27 +72,23 @@ __global__ void __launch_bounds__(kScrThreads) screen_write(const V *__restrict_
 
 }  // namespace
 
-void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev) {
-    if (k <= 0) {
-        cudaMemsetAsync(m_dev, 0, sizeof(int64_t), c.stream);
-        return;
-    }
+cudaError_t launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev) {
+    if (k <= 0) return cudaMemsetAsync(m_dev, 0, sizeof(int64_t), c.stream);
     const unsigned blocks = static_cast<unsigned>((k + kScrChunk - 1) / kScrChunk);
     screen_count<int64_t><<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count);
     screen_write<int64_t><<<blocks, kScrThreads, 0, c.stream>>>(c.f, k, t_floor, c.blk_count, c.surv, m_dev);
     c.launches += 2;
+    return cudaSuccess;
 }
 
 // real-valued f (a4'): survivors f_k > T compared in binary64
-void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev) {
-    if (k <= 0) {
-        cudaMemsetAsync(m_dev, 0, sizeof(int64_t), c.stream);
-        return;
-    }
+cudaError_t launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev) {
+    if (k <= 0) return cudaMemsetAsync(m_dev, 0, sizeof(int64_t), c.stream);
     const unsigned blocks = static_cast<unsigned>((k + kScrChunk - 1) / kScrChunk);
     screen_count<double><<<blocks, kScrThreads, 0, c.stream>>>(c.freal, k, T, c.blk_count);
     screen_write<double><<<blocks, kScrThreads, 0, c.stream>>>(c.freal, k, T, c.blk_count, c.surv, m_dev);
     c.launches += 2;
+    return cudaSuccess;
 }
 
 }  // namespace ubqp

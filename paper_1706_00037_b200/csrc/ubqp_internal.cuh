@@ -20,7 +20,21 @@ constexpr int kUmmaK = 32;        // K per tcgen05.mma kind::i8
 constexpr int kStages = 4;        // smem pipeline depth
 constexpr int kNPadAlign = 128;   // n_pad multiple (K dim of the GEMM)
 constexpr int kQRowAlign = kBN;   // Q8 rows padded to a multiple of the N tile
-constexpr int kSlices = 4;        // int8 limb planes of a real-valued Q (28-bit fixed point)
+constexpr int kSlices = 4;        // int8 limb planes of the real-Q walk image (28-bit, R20)
+constexpr int kMaxLimbs = 10;     // int8 limb planes of the real-Q evaluation image (R22)
+constexpr int kMaxPlanes = kMaxLimbs;
+
+// fold modes of the evaluation kernel (eval_tc.cu)
+enum { kFoldInt = 0, kFoldPlane = 1, kFoldReal = 2 };
+
+// One B operand of the evaluation GEMM: 1..kMaxPlanes int8 planes of Q (plane s weighs 128^s)
+struct Operand {
+    int planes = 0;
+    bool tri = false;                 // lower triangles: f-only triangular evaluation (NEXT-1)
+    CUtensorMap full[kMaxPlanes]{};   // 256-row B boxes (single-CTA kernel)
+    CUtensorMap half[kMaxPlanes]{};   // 128-row B boxes (CTA-pair kernel: each CTA half of N)
+    const int32_t *diag[kMaxPlanes]{};
+};
 
 struct Ctx {
     int device = 0;
@@ -36,6 +50,13 @@ struct Ctx {
     int8_t *Q8 = nullptr;        // [q_rows][q_ld] row-major, zero padded; row k = column k (Q = Q^t)
     int32_t *diag = nullptr;     // [q_rows]
     int qmax = 0;                // max |Q_ij| of the loaded integer Q
+    int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
+    Operand op_full, op_tri;     // integer Q: Q8 (gains) and Q8L (f only)
+    // sparse rows of the integer Q (NEXT-3): CSR without the diagonal, entries (j << 8 | (q & 0xFF))
+    int64_t nnz = 0;             // off-diagonal nonzeros
+    int32_t *csr_ptr = nullptr;  // [n + 1]
+    uint32_t *csr_ent = nullptr; // [nnz]
+    int asc_kernel = 0;          // 0 auto (by density), 1 dense, 2 sparse (UBQP_OPT_ASCENT)
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
     int64_t parents_cap = 0;
@@ -52,36 +73,68 @@ struct Ctx {
     int32_t *surv = nullptr;     // [k_max]
     int32_t *blk_count = nullptr;// screen block counts
     int64_t *scratch64 = nullptr;// small device scratch (stats, m, best key)
+    // in-kernel fold of the evaluation (eval_tc.cu): row partials, group counters and results
+    int32_t *part = nullptr;     // int32 partial row-dots, part_cap elements
+    int64_t part_cap = 0;
+    unsigned *grp_cnt = nullptr; // [grp_cap] self-resetting arrival counters (last one: groups done)
+    int64_t grp_cap = 0;
+    int64_t *grp_res = nullptr;  // [grp_cap][4]
     // ascent outputs scratch
     int64_t *asc_f = nullptr; int32_t *asc_flips = nullptr; uint64_t *asc_bits = nullptr;
     int32_t *asc_slots = nullptr; int32_t *asc_aux = nullptr; int64_t asc_cap = 0;
-    // TMA descriptors (64 B each, passed by value as __grid_constant__)
-    CUtensorMap tmap_X8{}, tmap_Q8{};
-    int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
-    CUtensorMap tmap_Q8L{};
-    // 128-row B boxes for the CTA-pair (cta_group::2) evaluation: each CTA loads half of N
-    CUtensorMap tmap_Q8_h{}, tmap_Q8L_h{};
-    CUtensorMap tmap_Qs_h[kSlices]{};
+    // TMA descriptor of the batch (A operand)
+    CUtensorMap tmap_X8{};
     bool eval_pair = true;       // UBQP_EVAL_2SM=0 selects the single-CTA kernel
     bool eval_attr_set = false, eval_pair_attr_set = false;   // dynamic-smem opt-in done
     bool sym_eval = true;        // f-only evaluations use the triangular GEMM (UBQP_FULL_EVAL disables)
-    // real-valued Q (a4'): Q~ = 2^-q_exp * sum_s 128^s L_s, int8 limb planes L_s in [-64, 63]
+    // real-valued Q (a4').  Evaluation image (R22): Qw~ = 2^-w_exp sum_s 128^s Lw_s with w_limbs
+    // int8 planes, exact for float32 Q and within 2^-32 relative per coefficient otherwise.
+    // Walk image (R20): Qt = rint(Q 2^q_exp), 28 bits, as 4 int8 planes (initial gains) and int32
+    // rows (the ascent streams them).
     bool real = false;
+    int w_exp = 0, w_limbs = 0;
+    int8_t *Qw[kMaxLimbs] = {};  // [q_rows][q_ld] full planes (first-derivative row sums)
+    int8_t *QwL[kMaxLimbs] = {}; // [q_rows][n_pad] lower triangles (f-only evaluation)
+    int32_t *wdiag = nullptr;    // [kMaxLimbs][q_rows] diagonal of each plane
+    Operand op_wide;             // QwL planes, tri
     int q_exp = 0;
-    int8_t *Qs[kSlices] = {nullptr, nullptr, nullptr, nullptr};
-    CUtensorMap tmap_Qs[kSlices]{};
-    int64_t *fs = nullptr;       // [kSlices][k_max] per-plane x^t L_s x
-    int64_t *fint = nullptr;     // [k_max] integer image f~ = sum_s 128^s f_s
-    double *freal = nullptr;     // [k_max] f = 2^-q_exp f~
-    // real-Q ascent (R20): the image Qt = rint(Q 2^e) as int32 rows [q_rows][qt_ld] (zero
-    // padded), its diagonal, and int64 gains of the batch
+    int8_t *Qs[kSlices] = {nullptr, nullptr, nullptr, nullptr};   // walk planes [q_rows][q_ld]
+    Operand op_walk[kSlices];    // one plane each (EMIT_GAINS launches), zero diagonal
+    int32_t *zdiag = nullptr;    // [q_rows] zeros
+    int64_t *fs = nullptr;       // [kSlices][k_max] per-walk-plane x^t L_s x
+    int64_t *fint = nullptr;     // [k_max] walk image f~28 = sum_s 128^s f_s
+    double *freal = nullptr;     // [k_max] f of the evaluation image
     int32_t *Qt = nullptr;
     int qt_ld = 0;
     int32_t *diagt = nullptr;    // [n_pad]
     int64_t *gains64 = nullptr;  // [k_max][n_pad]
     bool gains64_valid = false;
     bool freal_valid = false;
+    // re-evaluation workspace of ascended real-Q solutions (their f on the evaluation image)
+    int8_t *X8r = nullptr;       // [kReevalRows][n_pad]
+    CUtensorMap tmap_X8r{};
     int64_t launches = 0;
+};
+
+constexpr int64_t kReevalRows = 8192;   // rows per re-evaluation chunk of ascend_real
+
+// Shape of one evaluation launch (eval_tc.cu)
+struct EvalShape {
+    bool pair;
+    int num_n_tiles, num_k_blocks, ksplit, items_per_group;
+    int64_t num_m_tiles, mn_tiles, num_items, num_groups, part_ld, part_elems;
+};
+struct EvalLaunch {
+    const CUtensorMap *tmX = nullptr;  // A operand (batch X8 or the re-evaluation workspace)
+    const uint64_t *Xb = nullptr;      // packed bits of the same rows
+    int64_t k = 0;
+    const Operand *op = nullptr;
+    bool emit_gains = false;
+    int mode = kFoldInt;
+    int64_t *f = nullptr, *f2 = nullptr;
+    double *fr = nullptr, *fr2 = nullptr;
+    int64_t *stats = nullptr, *stats2 = nullptr;
+    int rank = 0, world = 1, q_exp = 0;
 };
 
 // ------------------------------------------------------------------ launchers (host)
@@ -91,16 +144,14 @@ void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k,
                    const uint64_t *parents_dev = nullptr, int64_t n_parents = 0);
 void launch_random(Ctx &c, uint64_t seed, int64_t k);
 void launch_expand(Ctx &c, int64_t k);     // Xb -> X8 (after set_batch)
-void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer or real planes
+void launch_expand_to(Ctx &c, const uint64_t *bits, int64_t k, int8_t *X8dst);   // any rows -> X8dst
+void launch_first_derivative(Ctx &c, uint64_t *bits_dev);   // integer Q8 or the real evaluation planes
 // eval_tc.cu
-// plane = -1: the integer Q8; plane >= 0: limb plane of a real-valued Q
-void launch_eval_tc(Ctx &c, int64_t k, bool emit_gains, int plane = -1, int64_t *f_out = nullptr,
-                    bool sym = false);
-void launch_stats(Ctx &c, int64_t k, int64_t *stats_dev);
-void launch_combine_real(Ctx &c, int64_t k, int64_t *stats_dev);
+EvalShape eval_shape(const Ctx &c, int64_t k, int planes, bool emit_gains, bool sym);
+int launch_eval(Ctx &c, const EvalLaunch &L);   // 1: fold buffers too small (size them first)
 // screen.cu
-void launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);
-void launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
+cudaError_t launch_screen(Ctx &c, int64_t k, int64_t t_floor, int64_t *m_dev);   // k <= 0: memset m
+cudaError_t launch_screen_real(Ctx &c, int64_t k, double T, int64_t *m_dev);
 // ascend_real.cu (R20)
 int real_qt_ld(int n_pad);
 void launch_gains_combine(Ctx &c, int64_t k, int plane);   // gains64 (+)= gains << 7 plane

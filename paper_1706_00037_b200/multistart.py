@@ -117,6 +117,7 @@ class MultiStart:
         self.k_local = len(range(self.rank, self.K, self.world))
         self.lam = float(lam)
         self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
+        self.qmax = int(np.abs(np.asarray(Q)).max()) if self.n else 0
         # one non-default stream shared by torch (collectives, small ops) and libubqp.so
         self.stream = torch.cuda.Stream(device=self.device)
         torch.cuda.set_stream(self.stream)
@@ -232,6 +233,13 @@ class MultiStart:
         pool[g mod P] (O4b) instead of Glover's generator.  polish_end: after the
         last round, polish(pool + [incumbent]); a strict improvement is recorded as round
         rounds + 1."""
+        if polish_end:
+            # fail before any round runs (not after all of them): the polish batch holds every
+            # ordered pair of pool + incumbent, and ubqp_relink needs (2n-1) qmax < 2^21
+            if (pool_cap + 1) * pool_cap > POLISH_MAX_PAIRS:
+                raise ValueError(f"polish_end: pool_cap {pool_cap} gives more than {POLISH_MAX_PAIRS} pairs")
+            if (2 * self.n - 1) * self.qmax >= (1 << 21):
+                raise ValueError("polish_end: path relinking needs (2n-1)*qmax < 2^21 (ubqp_relink E_RANGE)")
         mean = self.sample_mean(sample_seed)
         inc_bits, inc_f = self.first_derivative()
         if lam_policy == "paper":
@@ -258,12 +266,14 @@ class MultiStart:
         return inc_f, inc_bits, traj
 
 
-# ---------------------------------------------------------------- real-valued Q (R20)
+# ---------------------------------------------------------------- real-valued Q (R20, R22)
 def combine_real_stats(st, group=None):
-    """ubqp_stats_real of each rank -> (sum f~ as a Python int, count, max f~): one all_gather
-    of four int64 words per rank, combined exactly on the host (the sum is int128)."""
+    """ubqp_stats_real of each rank -> (sum f~ as a Python int, count, max f~ or None): one
+    all_gather of the six int64 words per rank, combined exactly on the host (int128 sums)."""
     _, world = dist_info(group)
-    words = torch.tensor([st.sum_hi, st.sum_lo, st.count, st.max_fint], dtype=torch.int64)
+    lo64 = lambda v: v - (1 << 64) if v >= (1 << 63) else v     # uint64 word -> int64 tensor value
+    words = torch.tensor([st.sum_hi, lo64(st.sum_lo), st.count, st.max_hi, lo64(st.max_lo), st.exp],
+                         dtype=torch.int64)
     if world > 1:
         dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
         words = words.to(dev)
@@ -272,13 +282,17 @@ def combine_real_stats(st, group=None):
         rows = [o.cpu().tolist() for o in out]
     else:
         rows = [words.tolist()]
-    total = sum((hi << 64) | (lo & (2**64 - 1)) for hi, lo, _, _ in rows)
-    return total, sum(r[2] for r in rows), max(r[3] for r in rows if r[2] > 0)
+    i128 = lambda hi, lo: (hi << 64) | (lo & (2**64 - 1))
+    total = sum(i128(r[0], r[1]) for r in rows)
+    maxes = [i128(r[3], r[4]) for r in rows if r[2] > 0]
+    return total, sum(r[2] for r in rows), (max(maxes) if maxes else None)
 
 
 class MultiStartReal:
-    """Figure 2 rounds on a real-valued Q (R20): decisions on the fixed-point image, f~ exact,
-    reported f = 2^-e f~.  Same sharding and exchange pattern as MultiStart."""
+    """Figure 2 rounds on a real-valued Q: objective values on the evaluation image (R22:
+    x^t Q x correctly rounded for float32 Q), the walk on the walk image (R20).  Mean is the
+    exact mean of the sampled values rounded once; Max, T and the best record are binary64.
+    Same sharding and exchange pattern as MultiStart."""
 
     def __init__(self, Q: np.ndarray, K: int, lam: float = 0.5, max_flips: int | None = None,
                  device: int | None = None, group=None):
@@ -295,48 +309,53 @@ class MultiStartReal:
         torch.cuda.set_stream(self.stream)
         self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
         self.u.load_Q_real(np.ascontiguousarray(Q), max(self.k_local, 1))
-        self.e = self.u.real_exp
+        self.e = self.u.real_exp          # walk image (R20)
+        self.w = self.u.eval_exp          # evaluation image (R22)
         self.W64 = self.u.W64
         dv = torch.device("cuda", self.device)
         kl = max(self.k_local, 1)
         self.st = ubqp_stats_real()
         self.surv = torch.zeros(kl, dtype=torch.int32, device=dv)
-        self.fint = torch.zeros(kl, dtype=torch.int64, device=dv)
+        self.fa = torch.zeros(kl, dtype=torch.float64, device=dv)
         self.flips = torch.zeros(kl, dtype=torch.int32, device=dv)
         self.bits = torch.zeros((kl, self.W64), dtype=torch.int64, device=dv)
         self.fd_bits = torch.zeros(self.W64, dtype=torch.int64, device=dv)
 
-    def sample_mean(self, seed: int):
+    def _value(self, fint: int) -> float:
+        """2^-w f~ rounded once to binary64"""
+        from fractions import Fraction
+        return float(Fraction(fint) / (Fraction(2) ** self.w))
+
+    def sample_mean(self, seed: int) -> float:
+        from fractions import Fraction
         self.u.random(seed, self.k_local, self.rank, self.world)
         self.u.eval_batch_real(None, self.st)
         total, count, _ = combine_real_stats(self.st, self.group)
-        return total, count
+        return float(Fraction(total, count) / (Fraction(2) ** self.w))
 
     def first_derivative(self):
         self.u.first_derivative(self.fd_bits)
         self.u.set_batch(self.fd_bits, 1, 0, 1)
         self.u.eval_batch_real(None, self.st)
-        return self.fd_bits.clone(), int(self.st.max_fint)
+        return self.fd_bits.clone(), self._value(self.st.max_fint)
 
-    def round(self, seed_bits, t0: int, inc_fint: int, mean_pair):
-        """-> (m on this rank, T, best f~ over all ranks or None, its bits)."""
-        import math
+    def round(self, seed_bits, t0: int, inc_f: float, mean: float):
+        """-> (m on this rank, T, best f over all ranks or None, its bits)."""
         u = self.u
         u.diversify(seed_bits, t0, self.k_local, self.rank, self.world)
         u.eval_batch_real(None, self.st)
         _, _, bmax = combine_real_stats(self.st, self.group)
-        mean = math.ldexp(mean_pair[0] / mean_pair[1], -self.e)
-        maxv = math.ldexp(float(max(inc_fint, bmax)), -self.e)
+        maxv = inc_f if bmax is None else max(inc_f, self._value(bmax))
         m, T = u.screen_real(self.lam, mean, maxv, self.surv)
         best = None
         if m > 0:
-            u.ascend_real(self.surv, m, self.max_flips, None, self.fint, self.flips, self.bits)
-            fi = self.fint[:m]
-            mx = int(fi.max().item())
-            i = int(torch.nonzero(fi == mx)[0].item())      # lowest slot = lowest g among ties
+            u.ascend_real(self.surv, m, self.max_flips, self.fa, None, self.flips, self.bits)
+            fa = self.fa[:m]
+            mx = float(fa.max().item())
+            i = int(torch.nonzero(fa == mx)[0].item())      # lowest slot = lowest g among ties
             best = (mx, self.rank + int(self.surv[i].item()) * self.world, i)
-        # global best: highest f~, then lowest g; the owner broadcasts the bits
-        cand = torch.tensor([best[0], best[1]] if best else [-(2**62), 2**62], dtype=torch.int64)
+        # global best: highest f, then lowest g; the owner broadcasts the bits
+        cand = torch.tensor([best[0], float(best[1])] if best else [float("-inf"), float(2**62)], dtype=torch.float64)
         if self.world > 1:
             dev = self.bits.device if dist.get_backend(self.group) == "nccl" else "cpu"
             cand = cand.to(dev)
@@ -346,8 +365,9 @@ class MultiStartReal:
         else:
             rows = [cand.tolist()]
         gf, gg = max(rows, key=lambda r: (r[0], -r[1]))
-        if gf == -(2**62):
+        if gf == float("-inf"):
             return m, T, None, None
+        gg = int(gg)
         owner = gg % self.world
         row = self.bits[best[2]].clone() if (best and owner == self.rank) else torch.zeros_like(self.bits[0])
         if self.world > 1:

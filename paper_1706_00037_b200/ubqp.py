@@ -25,9 +25,12 @@ Q_N, Q_NPAD, Q_W64, Q_KMAX, Q_KLOCAL, Q_LAUNCHES, Q_STREAM = range(7)
 EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ubqp_load_Q",
            "ubqp_diversify", "ubqp_blend", "ubqp_random", "ubqp_first_derivative", "ubqp_set_batch", "ubqp_get_batch", "ubqp_eval_batch",
            "ubqp_get_gains", "ubqp_screen", "ubqp_ascend", "ubqp_relink", "ubqp_sync", "ubqp_query",
-           "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real", "ubqp_ascend_real"]
+           "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real", "ubqp_ascend_real",
+           "ubqp_set_option"]
 UBQP_F32, UBQP_F64 = 1, 2
-Q_REAL_EXP, Q_IS_REAL = 7, 8
+Q_REAL_EXP, Q_IS_REAL, Q_EVAL_EXP, Q_EVAL_LIMBS, Q_NNZ, Q_SPARSE_ROWS = 7, 8, 9, 10, 11, 12
+OPT_ASCENT, OPT_EVAL_PAIR, OPT_EVAL_TRI = 0, 1, 2
+ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE = 0, 1, 2
 
 
 class UbqpError(RuntimeError):
@@ -37,13 +40,18 @@ class UbqpError(RuntimeError):
 
 
 class ubqp_stats_real(ctypes.Structure):
-    """integer-image statistics of a real-Q batch (include/ubqp.h)"""
-    _fields_ = [("sum_hi", ctypes.c_int64), ("sum_lo", ctypes.c_int64), ("count", ctypes.c_int64),
-                ("max_fint", ctypes.c_int64)]
+    """statistics of a real-Q batch on the evaluation image (include/ubqp.h): f~ = f 2^exp"""
+    _fields_ = [("sum_hi", ctypes.c_int64), ("sum_lo", ctypes.c_uint64), ("count", ctypes.c_int64),
+                ("max_hi", ctypes.c_int64), ("max_lo", ctypes.c_uint64), ("exp", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     @property
     def sum_fint(self) -> int:
-        return (self.sum_hi << 64) | (self.sum_lo & (2**64 - 1))
+        return (self.sum_hi << 64) | self.sum_lo
+
+    @property
+    def max_fint(self) -> int:
+        return (self.max_hi << 64) | self.max_lo
 
 
 class ubqp_stats(ctypes.Structure):
@@ -85,6 +93,7 @@ def load_library(path: Path | str | None = None):
         "ubqp_eval_batch_real": ([P, P, P], ctypes.c_int),
         "ubqp_screen_real": ([P, dbl, dbl, dbl, P, P, P], ctypes.c_int),
         "ubqp_ascend_real": ([P, P, i64, i32, P, P, P, P], ctypes.c_int),
+        "ubqp_set_option": ([P, ctypes.c_int, i64], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -211,7 +220,20 @@ class Ubqp:
 
     @property
     def real_exp(self) -> int:
+        """exponent e of the walk image Qt = rint(Q 2^e) (R20)"""
         return self.query(Q_REAL_EXP)
+
+    @property
+    def eval_exp(self) -> int:
+        """exponent w of the evaluation image (R22)"""
+        return self.query(Q_EVAL_EXP)
+
+    @property
+    def eval_limbs(self) -> int:
+        return self.query(Q_EVAL_LIMBS)
+
+    def set_option(self, what: int, value: int):
+        self._ck(self.lib.ubqp_set_option(self.h, what, int(value)))
 
     def eval_batch_real(self, f_out=None, stats_out=None):
         self._ck(self.lib.ubqp_eval_batch_real(self.h, _ptr(f_out), _ptr(stats_out)))

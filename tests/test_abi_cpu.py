@@ -52,7 +52,7 @@ def test_library_is_sm100a_native():
 
 def test_version_and_null_handle(lib):
     lib.ubqp_version.restype = ctypes.c_int
-    assert lib.ubqp_version() == 103
+    assert lib.ubqp_version() == 200
     lib.ubqp_last_error.restype = ctypes.c_char_p
     lib.ubqp_last_error.argtypes = [ctypes.c_void_p]
     assert b"null" in lib.ubqp_last_error(None)

@@ -67,8 +67,8 @@ def _worker_real(rank, world, port, n, K, rounds, lam, out):
         torch.cuda.set_device(0)
         from paper_1706_00037_b200.multistart import MultiStartReal
         rng = np.random.default_rng(n)
-        A = rng.uniform(-30, 30, size=(n, n))
-        Q = np.triu(A) + np.triu(A, 1).T
+        A = rng.uniform(-30, 30, size=(n, n)).astype(np.float32)   # exactly represented (R22)
+        Q = (np.triu(A) + np.triu(A, 1).T).astype(np.float64)
         ms = MultiStartReal(Q, K, lam=lam, max_flips=10 * n, device=0)
         best, bits, traj = ms.run(rounds, sample_seed=4)
         out[rank] = (best, traj, bits.cpu().numpy().tobytes())
@@ -77,14 +77,14 @@ def _worker_real(rank, world, port, n, K, rounds, lam, out):
 
 
 def test_sharded_real_rounds_match_single_rank_oracle():
-    """MultiStartReal (R20) on 2 ranks: int128 stats exchange, best (f~, g) record, owner bits."""
+    """MultiStartReal (R20, R22) on 2 ranks: int128 stats exchange, best (f, g) record, owner bits."""
     n, K, rounds, lam, world = 150, 900, 3, 0.35, 2
     mgr = mp.Manager()
     out = mgr.dict()
     mp.spawn(_worker_real, args=(world, _port(), n, K, rounds, lam, out), nprocs=world, join=True)
     rng = np.random.default_rng(n)
-    A = rng.uniform(-30, 30, size=(n, n))
-    Q = np.triu(A) + np.triu(A, 1).T
+    A = rng.uniform(-30, 30, size=(n, n)).astype(np.float32)
+    Q = (np.triu(A) + np.triu(A, 1).T).astype(np.float64)
     ob, ox, otraj, e = oracle.run_rounds_real(Q, K, rounds, lam, 10 * n, sample_seed=4, nthreads=8)
     for r in range(world):
         best, traj, bits = out[r]

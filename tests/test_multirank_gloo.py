@@ -121,14 +121,14 @@ def _worker_real(rank, world, port, out):
         class St:                                   # the ubqp_stats_real fields of one rank
             pass
         rng = np.random.default_rng(100 + rank)
-        v = [int(x) for x in rng.integers(-(2**60), 2**60, size=5)] if rank != 1 else []
+        v = [int(x) << 40 for x in rng.integers(-(2**60), 2**60, size=5)] if rank != 1 else []   # int128 values
         total = sum(v)
         st = St()
-        st.sum_hi, st.sum_lo = total >> 64, total & (2**64 - 1)
-        if st.sum_lo >= 2**63:
-            st.sum_lo -= 2**64                      # the C struct stores a signed int64 word
+        st.sum_hi, st.sum_lo = total >> 64, total & (2**64 - 1)     # uint64 low word, as in the C struct
         st.count = len(v)
-        st.max_fint = max(v) if v else -(2**63)
+        mx = max(v) if v else -(2**127)
+        st.max_hi, st.max_lo = mx >> 64, mx & (2**64 - 1)
+        st.exp = 7
         out[rank] = combine_real_stats(st)
     finally:
         dist.destroy_process_group()
@@ -143,6 +143,6 @@ def test_real_stats_exchange_is_exact(world):
     vals = []
     for r in range(world):
         if r != 1:
-            vals += [int(x) for x in np.random.default_rng(100 + r).integers(-(2**60), 2**60, size=5)]
+            vals += [int(x) << 40 for x in np.random.default_rng(100 + r).integers(-(2**60), 2**60, size=5)]
     for r in range(world):
         assert out[r] == (sum(vals), len(vals), max(vals))

@@ -603,19 +603,53 @@ def test_real_ascent_value_within_rounding_bound():
 
 
 def test_real_rounds_integer_Q_reduce_to_integer_rounds_and_world_invariance():
-    # integer-valued real Q (max |Q| = 100): the image is 2^20 Q, so every decision equals
-    # the integer round loop's and f~ = 2^20 f (same trajectory rounds)
+    # integer-valued real Q: every O9 value is the integer O1 value and the walk image is 2^20 Q
+    # (max |Q| = 100), so every decision equals the integer round loop's
     Q = generate_Q(60, 0.5, -100, 100, seed=71).astype(np.int32)
     Q[0, 0] = 100
     a = oracle.run_rounds(Q, K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3)
     b = oracle.run_rounds_real(Q.astype(np.float64), K=50, rounds=3, lam=0.4, max_flips=600, sample_seed=3)
-    assert b[3] == 20 and b[0] == a[0] * 2**20 and np.array_equal(b[1], a[1])
-    assert [(r, v) for r, v in b[2]] == [(r, v * 2**20) for r, v in a[2]]
+    assert b[3] == 20 and b[0] == a[0] and np.array_equal(b[1], a[1])
+    assert b[2] == a[2]
     rng = np.random.default_rng(72)
     A = rng.uniform(-10, 10, size=(45, 45))
     Qr = np.triu(A) + np.triu(A, 1).T
     c = oracle.run_rounds_real(Qr, K=40, rounds=3, lam=0.3, max_flips=500, sample_seed=4)
     d = oracle.run_rounds_real(Qr, K=40, rounds=3, lam=0.3, max_flips=500, sample_seed=4, world=3)
     assert c[0] == d[0] and np.array_equal(c[1], d[1]) and c[2] == d[2]
-    Qt, e = oracle.real_image(Qr)
-    assert c[0] == oracle.xQx(Qt.astype(np.int32), c[1])
+    assert c[0] == oracle.xQx_real(Qr, c[1])
+    assert [v for _, v in c[2]] == sorted(v for _, v in c[2]) and len(set(v for _, v in c[2])) == len(c[2])
+
+
+def test_real_gains_brute_force_exact():
+    """gains_real is the exactly rounded f(x xor e_j) - f(x): checked with exact rationals
+    (fractions) on values that are not representable in a short fixed point."""
+    from fractions import Fraction
+    rng = np.random.default_rng(81)
+    n = 9
+    A = rng.standard_normal((n, n)) * np.exp2(rng.integers(-30, 30, size=(n, n)))
+    Q = np.triu(A) + np.triu(A, 1).T
+    for t in range(6):
+        x = rng.integers(0, 2, size=n).astype(np.uint8)
+
+        def fx(y):
+            S = np.flatnonzero(y)
+            return sum((Fraction(Q[i, j]) for i in S for j in S), Fraction(0))
+
+        g = oracle.gains_real(Q, x)
+        f0 = fx(x)
+        for j in range(n):
+            y = x.copy()
+            y[j] ^= 1
+            assert g[j] == float(fx(y) - f0), (t, j)
+
+
+def test_batch_sum_exact_matches_fraction_sums():
+    from fractions import Fraction
+    rng = np.random.default_rng(82)
+    n, K = 7, 13
+    A = rng.uniform(-1, 1, size=(n, n)) * 1e-3 + 1e6
+    Q = np.triu(A) + np.triu(A, 1).T
+    X = rng.integers(0, 2, size=(K, n)).astype(np.uint8)
+    want = sum((Fraction(Q[i, j]) for x in X for i in np.flatnonzero(x) for j in np.flatnonzero(x)), Fraction(0))
+    assert oracle.batch_sum_exact(Q, X) == want
