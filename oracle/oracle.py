@@ -259,7 +259,7 @@ def polish(Q, elite, max_flips: int, nthreads: int = 1):
 # O8 -- batched rounds of Figure 2 (R5, R6, R13)
 def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
                world: int = 1, nthreads: int = 1, div: str = "glover", pool_cap: int = 8,
-               polish_end: bool = False):
+               polish_end: bool = False, trace: list | None = None):
     """Round 0: K random starts (O3, seed ``sample_seed``) -> pinned (mean_sum, mean_count)
     (P:55 "the mean is the average xQx value derived during sampling").  Incumbent =
     first-derivative start.  Round r >= 1: diversify from the incumbent with
@@ -270,7 +270,8 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
     ``div`` "blend": once the parent pool (pool_update) is non-empty, rounds blend the
     incumbent with pool[g mod P] (O4b) instead of O4.  ``polish_end``: after the last
     round, polish(pool + [incumbent]) (O11 + O7); a strictly better result is recorded as
-    round ``rounds + 1``.
+    round ``rounds + 1``.  ``trace`` (a list) receives one dict per round: t0, the batch f,
+    Max, T, the survivors (global g), the ascended (g, f) pairs, the round's best (f, g, x).
     Returns (best_value, best_x, trajectory[list of (round, best_value)])."""
     Q = _Q(Q)
     n = Q.shape[0]
@@ -301,15 +302,26 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
         fs = [eval_batch(Q, Xr, nthreads) for Xr in Xs]
         batch_max = max(int(fr.max()) for fr in fs if fr.size)
         T = threshold(lam, mean_sum, mean_count, max(inc_f, batch_max))
+        tr = {"round": rnd, "t0": t0, "mean_sum": mean_sum, "mean_count": mean_count,
+              "max_value": max(inc_f, batch_max), "T": T, "survivors": [], "ascended": []}
         for r in range(world):
             s = screen(fs[r], T)
+            tr["survivors"] += [r + int(v) * world for v in s]
             if s.size == 0:
                 continue
             Xa, fa, _ = ascend(Q, Xs[r][s], fs[r][s], max_flips, nthreads)
             for i, slot in enumerate(s):
                 key = max_key(int(fa[i]), r + int(slot) * world)
+                tr["ascended"].append((r + int(slot) * world, int(fa[i])))
                 if key > best_key:
                     best_key, best = key, (int(fa[i]), Xa[i].copy())
+        if trace is not None:
+            tr["survivors"].sort()
+            tr["ascended"].sort()
+            tr["f"] = [int(v) for g in range(K) for v in [fs[g % world][g // world]]]
+            tr["best"] = None if best is None else (best[0], (1 << 22) - 1 - (best_key & ((1 << 22) - 1)),
+                                                     best[1].copy())
+            trace.append(tr)
         improved_from = None
         if best is not None and best[0] > inc_f:
             improved_from = inc_x

@@ -653,3 +653,72 @@ def test_batch_sum_exact_matches_fraction_sums():
     X = rng.integers(0, 2, size=(K, n)).astype(np.uint8)
     want = sum((Fraction(Q[i, j]) for x in X for i in np.flatnonzero(x) for j in np.flatnonzero(x)), Fraction(0))
     assert oracle.batch_sum_exact(Q, X) == want
+
+
+# ---------------------------------------------------------------- O8 hand-worked trace
+def _read_rounds_golden():
+    g = {"Q": [], "sample": [], "rounds": {}}
+    for line in (GOLD / "rounds_n5.txt").read_text().splitlines():
+        if not line.strip() or line.startswith("#"):
+            continue
+        tok = line.split()
+        key = tok[0]
+        if key == "Q":
+            g["Q"].append([int(v) for v in tok[1:]])
+        elif key == "sample":
+            g["sample"].append(([int(c) for c in tok[1]], int(tok[2])))
+        elif key in ("K", "n_rounds", "sample_seed", "mean_sum", "mean_count"):
+            g[key] = int(tok[1])
+        elif key == "lambda":
+            g[key] = float(tok[1])
+        elif key == "start":
+            g["start"] = ([int(c) for c in tok[1]], int(tok[2]))
+        else:
+            r = int(tok[1])
+            d = g["rounds"].setdefault(r, {})
+            if key == "round":
+                d["t0"] = int(tok[3])
+            elif key in ("f", "survivors"):
+                d[key] = [int(v) for v in tok[2:]]
+            elif key == "max_value":
+                d[key] = int(tok[2])
+            elif key == "ascended":
+                d[key] = [tuple(int(v) for v in p.split(":")) for p in tok[2:]]
+            elif key == "best":
+                d[key] = (int(tok[2]), int(tok[3]), [int(c) for c in tok[4]])
+            elif key == "incumbent":
+                d[key] = (int(tok[2]), [int(c) for c in tok[3]])
+    return g
+
+
+def test_rounds_hand_worked_trace():
+    """O8 against a hand-worked n = 5 trace (tests/golden/rounds_n5.txt): t0 = (r-1)K, the
+    pinned sampling mean, Max = max(incumbent, batch max), ties to the lowest g, strict
+    update -- each a reading the trace distinguishes from its plausible alternative."""
+    g = _read_rounds_golden()
+    Q = np.array(g["Q"], dtype=np.int32)
+    n, K = Q.shape[0], g["K"]
+    S = oracle.random_solutions(n, g["sample_seed"], K)
+    for (x, fv), row in zip(g["sample"], S):
+        assert row.tolist() == x and oracle.xQx(Q, row) == fv
+    assert sum(fv for _, fv in g["sample"]) == g["mean_sum"] and K == g["mean_count"]
+    assert oracle.first_derivative_start(Q).tolist() == g["start"][0]
+    trace = []
+    best, bx, traj = oracle.run_rounds(Q, K, g["n_rounds"], g["lambda"], 50, g["sample_seed"], trace=trace)
+    assert len(trace) == g["n_rounds"]
+    inc = g["start"]
+    for tr in trace:
+        want = g["rounds"][tr["round"]]
+        assert tr["t0"] == want["t0"]
+        assert (tr["mean_sum"], tr["mean_count"]) == (g["mean_sum"], g["mean_count"])
+        assert tr["f"] == want["f"] and tr["max_value"] == want["max_value"]
+        mean = g["mean_sum"] / g["mean_count"]
+        assert tr["T"] == mean + g["lambda"] * (want["max_value"] - mean)
+        assert tr["survivors"] == want["survivors"] and tr["ascended"] == want["ascended"]
+        bf, bg, bxx = tr["best"]
+        assert (bf, bg, bxx.tolist()) == want["best"]
+        if bf > inc[1]:
+            inc = (bxx.tolist(), bf)
+        assert (inc[1], inc[0]) == want["incumbent"]
+    assert best == inc[1] and bx.tolist() == inc[0]
+    assert traj == [(0, g["start"][1]), (1, 42)]
