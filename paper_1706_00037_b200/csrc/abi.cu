@@ -691,6 +691,8 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, in
     uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
     int64_t *k_d = k_dev ? best_key_out : h->scratch64 + 5;
     CK(cudaMemsetAsync(k_d, 0xFF, sizeof(int64_t), h->stream));     // -1 = none
+    if (h->asc_kernel == 2 && !h->csr_ptr)
+        return fail(h, UBQP_E_STATE, "ubqp: sparse ascent requested but the sparse rows were not built (density > 0.25)");
     if (ubqp::launch_ascend(*h, slots_dev, m, max_flips, f_d, fl_d, b_d, k_d))
         return fail(h, UBQP_E_RANGE, "ubqp: n outside the ascent kernel range");
     CK_LAUNCH("ascend_kernel");

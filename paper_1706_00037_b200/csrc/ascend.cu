@@ -482,8 +482,16 @@ static int launch_walk(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_
     return 1;
 }
 
+bool ascent_uses_sparse(const Ctx &c) {
+    if (c.asc_kernel == 2) return true;
+    if (c.asc_kernel == 1 || !c.csr_ptr || c.n < 2) return false;
+    return static_cast<double>(c.nnz) <= kSparseAutoDensity * c.n * (c.n - 1.0);
+}
+
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                   int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
+    if (ascent_uses_sparse(c))
+        return launch_ascend_sparse(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);
     return launch_walk(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev, nullptr);
 }
 

@@ -161,6 +161,12 @@ int launch_ascend_real(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_
 int ascend_capacity(int n_pad);   // variables covered by the default ascent shape (>= n_pad)
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips,
                   int64_t *f_dev, int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
+// ascend_sparse.cu (NEXT-3): the same walk on CSR rows; 1 if the rows were not built / too large
+int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
+                         int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
+// off-diagonal density at or below which UBQP_OPT_ASCENT = 0 picks the sparse kernel (measured crossover)
+constexpr double kSparseAutoDensity = 0.15;
+bool ascent_uses_sparse(const Ctx &c);
 // path relinking (O11) of batch slots toward guides[i mod n_guides] on the ascent kernel
 int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
                   int64_t *f_dev, int32_t *steps_dev, int32_t *sbest_dev, int32_t *len_dev, uint64_t *bits_dev,

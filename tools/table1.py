@@ -23,5 +23,19 @@ for n, dens, sq in ((2500, 0.1, 2), (5000, 1.0, 3), (7000, 1.0, 4)):
         u.eval_batch(0, f)
     e1.record()
     torch.cuda.synchronize()
-    print(n, f"{e0.elapsed_time(e1) / 50 * 1e3:.1f} us per 1000 evals", int(f.sum().item()), flush=True)
+    api_us = e0.elapsed_time(e1) / 50 * 1e3
+    # the same 50 calls captured in a CUDA graph: device time without host launch overhead
+    st = torch.zeros(4, dtype=torch.int64, device="cuda")
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
+        for _ in range(50):
+            u.eval_batch(0, f, st)
+    g.replay()
+    torch.cuda.synchronize()
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    print(n, f"{api_us:.1f} us per 1000 evals (API calls), {e0.elapsed_time(e1) / 50 * 1e3:.1f} us (graph replay)",
+          int(f.sum().item()), st.tolist(), flush=True)
     u.close()
