@@ -268,7 +268,7 @@ int ubqp_sync(ubqp_t h);
 /* Introspection (read-only): n, n_pad, W64, k_max, k_local, kernels launched so far, the
  * stream, the walk-image exponent e (R20), 1 if a real Q is loaded, the evaluation-image
  * exponent w and limb count L (R22; integer Q: 0 and 1), the off-diagonal nonzeros of an
- * integer Q, 1 if its sparse rows (CSR, NEXT-3) were built (off-diagonal density <= 0.25). */
+ * integer Q, 1 if its sparse rows (fixed-stride ELL rows, NEXT-3) were built (off-diagonal density <= 0.25). */
 enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
        UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8,
        UBQP_Q_EVAL_EXP = 9, UBQP_Q_EVAL_LIMBS = 10, UBQP_Q_NNZ = 11, UBQP_Q_SPARSE_ROWS = 12 };

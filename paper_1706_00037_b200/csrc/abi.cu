@@ -85,8 +85,9 @@ void free_batch(Ctx &c) {
 void free_all(Ctx &c) {
     free_batch(c);
     dfree(c.Q8); dfree(c.Q8L); dfree(c.diag); dfree(c.seed); dfree(c.parents); dfree(c.guides);
-    dfree(c.csr_ptr); dfree(c.csr_ent);
+    dfree(c.ell);
     c.nnz = 0;
+    c.ell_stride = 0;
     c.parents_cap = c.guides_cap = 0; dfree(c.scratch64);
     for (int s = 0; s < ubqp::kSlices; ++s) dfree(c.Qs[s]);
     for (int s = 0; s < ubqp::kMaxLimbs; ++s) { dfree(c.Qw[s]); dfree(c.QwL[s]); }
@@ -186,35 +187,39 @@ int eval_launch(ubqp_t h, const ubqp::EvalLaunch &L) {
     return UBQP_OK;
 }
 
-// CSR rows of Q without the diagonal for the sparse ascent (NEXT-3), built when the
-// off-diagonal density is at most kSparseBuildDensity; entries (j << 8) | (Q_kj & 0xFF), j ascending
+// Fixed-stride rows of Q without the diagonal for the sparse ascent (NEXT-3), built when the
+// off-diagonal density is at most kSparseBuildDensity: entries (j << 8) | (Q_kj & 0xFF), j
+// ascending, padded with 0xFFFFFFFF to the longest row rounded up to 32 entries
 constexpr double kSparseBuildDensity = 0.25;
 int build_sparse(ubqp_t h, const int32_t *Qh) {
     const int n = h->n;
     int64_t nnz = 0;
-    for (int64_t e = 0; e < static_cast<int64_t>(n) * n; ++e) nnz += Qh[e] != 0;
-    for (int i = 0; i < n; ++i) nnz -= Qh[static_cast<int64_t>(i) * n + i] != 0;
+    int maxrow = 0;
+    for (int i = 0; i < n; ++i) {
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += (j != i && Qh[static_cast<int64_t>(i) * n + j] != 0);
+        nnz += r;
+        maxrow = std::max(maxrow, r);
+    }
     h->nnz = nnz;
     if (n < 2 || static_cast<double>(nnz) > kSparseBuildDensity * n * (n - 1.0)) return UBQP_OK;
-    std::vector<int32_t> ptr(n + 1, 0);
-    std::vector<uint32_t> ent(nnz > 0 ? nnz : 1);
-    int64_t at = 0;
+    const int stride = std::max(32, (maxrow + 31) / 32 * 32);
+    std::vector<uint32_t> ent(static_cast<size_t>(n) * stride, 0xFFFFFFFFu);
     for (int i = 0; i < n; ++i) {
-        ptr[i] = static_cast<int32_t>(at);
+        int at = 0;
         for (int j = 0; j < n; ++j) {
             const int32_t v = Qh[static_cast<int64_t>(i) * n + j];
-            if (j != i && v != 0) ent[at++] = (static_cast<uint32_t>(j) << 8) | (static_cast<uint32_t>(v) & 0xFFu);
+            if (j != i && v != 0)
+                ent[static_cast<size_t>(i) * stride + at++] = (static_cast<uint32_t>(j) << 8) | (static_cast<uint32_t>(v) & 0xFFu);
         }
     }
-    ptr[n] = static_cast<int32_t>(at);
-    if (cudaMalloc(&h->csr_ptr, ptr.size() * sizeof(int32_t)) != cudaSuccess ||
-        cudaMalloc(&h->csr_ent, ent.size() * sizeof(uint32_t)) != cudaSuccess) {
+    if (cudaMalloc(&h->ell, ent.size() * sizeof(uint32_t)) != cudaSuccess) {
         cudaGetLastError();
         free_all(*h);
         return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the sparse rows of Q");
     }
-    CK(cudaMemcpy(h->csr_ptr, ptr.data(), ptr.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->csr_ent, ent.data(), ent.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    h->ell_stride = stride;
+    CK(cudaMemcpy(h->ell, ent.data(), ent.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
     return UBQP_OK;
 }
 
@@ -691,7 +696,7 @@ int ubqp_ascend(ubqp_t h, const int32_t *slots, int64_t m, int32_t max_flips, in
     uint64_t *b_d = b_dev ? bits_out : (bits_out ? h->asc_bits : nullptr);
     int64_t *k_d = k_dev ? best_key_out : h->scratch64 + 5;
     CK(cudaMemsetAsync(k_d, 0xFF, sizeof(int64_t), h->stream));     // -1 = none
-    if (h->asc_kernel == 2 && !h->csr_ptr)
+    if (h->asc_kernel == 2 && !h->ell)
         return fail(h, UBQP_E_STATE, "ubqp: sparse ascent requested but the sparse rows were not built (density > 0.25)");
     if (ubqp::launch_ascend(*h, slots_dev, m, max_flips, f_d, fl_d, b_d, k_d))
         return fail(h, UBQP_E_RANGE, "ubqp: n outside the ascent kernel range");
@@ -1068,7 +1073,7 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
         case UBQP_Q_EVAL_EXP: *value = h->real ? h->w_exp : 0; break;
         case UBQP_Q_EVAL_LIMBS: *value = h->real ? h->w_limbs : 1; break;
         case UBQP_Q_NNZ: *value = h->nnz; break;
-        case UBQP_Q_SPARSE_ROWS: *value = h->csr_ptr ? 1 : 0; break;
+        case UBQP_Q_SPARSE_ROWS: *value = h->ell ? 1 : 0; break;
         default: return UBQP_E_INVALID;
     }
     return UBQP_OK;

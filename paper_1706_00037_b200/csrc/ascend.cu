@@ -484,7 +484,7 @@ static int launch_walk(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_
 
 bool ascent_uses_sparse(const Ctx &c) {
     if (c.asc_kernel == 2) return true;
-    if (c.asc_kernel == 1 || !c.csr_ptr || c.n < 2) return false;
+    if (c.asc_kernel == 1 || !c.ell || c.n < 2) return false;
     return static_cast<double>(c.nnz) <= kSparseAutoDensity * c.n * (c.n - 1.0);
 }
 

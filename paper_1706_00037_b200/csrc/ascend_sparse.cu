@@ -12,8 +12,12 @@
 //     with a shared atomicMax when a gain rises, and rescanned (one warp-wide REDUX) only when
 //     the segment's own maximum falls -- on average nnz/64 + 1 segments per step;
 //   * the global argmax is a warp reduction over the segment keys (largest gain, lowest j);
-//   * row k* is read from CSR rows without the diagonal, entries (j << 8) | (Q_kj & 0xFF)
-//     (4 bytes per nonzero, L2-resident), one coalesced pass per step.
+//   * row k* is read from fixed-stride (ELL) rows without the diagonal, entries
+//     (j << 8) | (Q_kj & 0xFF), padded with 0xFFFFFFFF to the longest row rounded to 32 (4 bytes
+//     per nonzero, L2-resident): the row address needs no pointer load, and every entry of the
+//     row is loaded into registers at once (one L2 round trip per step); then all its gains are
+//     read, updated and written back as independent shared-memory accesses (the columns of a
+//     row are distinct).
 // Bound: latency of the dependent chain per step (argmax -> row k* from L2 -> scattered
 // shared-memory updates -> rescans), hidden by the warps resident per SM (shared memory:
 // 4 n + n/8 bytes per solution).  Algorithmic bytes per step: 4 nnz(row k*).
@@ -24,22 +28,22 @@
 namespace ubqp {
 namespace {
 
-constexpr int kSW = 4;   // warps (= solutions) per CTA
-
 __device__ __forceinline__ int seg_key(int g, int lane) {   // g = 2 Delta + x
     return (g >> 1) * 32 + (31 - lane);
 }
 
-__global__ void __launch_bounds__(32 * kSW)
+// R = ELL entries per lane held in registers per pass (stride <= 32 R: one pass per step)
+template <int R>
+__global__ void __launch_bounds__(128)
 ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n, int n_pad, int W64,
-                     int64_t k_local, int rank, int world, const int32_t *__restrict__ csr_ptr,
-                     const uint32_t *__restrict__ csr_ent, const int32_t *__restrict__ gains,
-                     const int64_t *__restrict__ f_in, const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out,
-                     int32_t *__restrict__ flips_out, uint64_t *__restrict__ bits_out,
-                     long long *__restrict__ best_key, int nseg, int words_per_warp) {
+                     int64_t k_local, int rank, int world, int stride, const uint32_t *__restrict__ ell,
+                     const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
+                     const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out, int32_t *__restrict__ flips_out,
+                     uint64_t *__restrict__ bits_out, long long *__restrict__ best_key, int nseg,
+                     int words_per_warp) {
     extern __shared__ int s_mem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * kSW + warp;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp;
     if (i >= m) return;
     int *G = s_mem + static_cast<int64_t>(warp) * words_per_warp;   // [nseg * 32]
     int *segkey = G + nseg * 32;                                    // [nseg]
@@ -74,41 +78,53 @@ ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips
         int bv = INT_MIN, bj = INT_MAX;
         for (int sg = lane; sg < nseg; sg += 32) {
             const int key = segkey[sg];
-            if (key == INT_MIN) continue;
             const int v = key >> 5;                               // floor: Delta
             const int j = sg * 32 + 31 - (key & 31);
-            if (v > bv || (v == bv && j < bj)) { bv = v; bj = j; }
+            if (key != INT_MIN && (v > bv || (v == bv && j < bj))) { bv = v; bj = j; }
         }
         const int gv = __reduce_max_sync(0xFFFFFFFFu, bv);
-        const int kstar = static_cast<int>(__reduce_min_sync(0xFFFFFFFFu, bv == gv ? static_cast<unsigned>(bj) : 0xFFFFFFFFu));
+        const int kstar =
+            static_cast<int>(__reduce_min_sync(0xFFFFFFFFu, bv == gv ? static_cast<unsigned>(bj) : 0xFFFFFFFFu));
         if (gv <= 0 || flips == max_flips) break;
 
-        // ---- flip k*
+        // ---- flip k*: the entries of row k* go to registers first (independent loads)
+        const uint32_t *row = ell + static_cast<int64_t>(kstar) * stride;
         const int gk = G[kstar];
         const int xk = gk & 1;
         const int d2 = xk ? -2 : 2;            // 2 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;
-        __syncwarp();
-        if (lane == 0) {
-            G[kstar] = 2 * (-gv) + (xk ^ 1);   // Delta_k* -> -Delta_k*, x_k* flipped
-            atomicOr(&dirty[(kstar >> 5) >> 5], 1u << ((kstar >> 5) & 31));   // its segment max fell
-        }
-        const int e0 = csr_ptr[kstar], e1 = csr_ptr[kstar + 1];
-        for (int e = e0 + lane; e < e1; e += 32) {
-            const uint32_t ent = __ldg(csr_ent + e);
-            const int j = static_cast<int>(ent >> 8);
-            const int q = static_cast<int>(static_cast<int8_t>(ent & 0xFFu));
-            const int g = G[j];
-            const int xj = g & 1;
-            const int delta = (xj ? -d2 : d2) * q;                 // 2 d (1 - 2 x_j) Q_jk*
-            const int ng = g + 2 * delta;
-            G[j] = ng;
-            const int sg = j >> 5, lj = j & 31;
-            if (delta > 0) {
-                atomicMax(&segkey[sg], seg_key(ng, lj));
-            } else if (delta < 0 && segkey[sg] == seg_key(g, lj)) {
-                atomicOr(&dirty[sg >> 5], 1u << (sg & 31));        // the segment's own max fell
+        for (int base = 0; base < stride; base += 32 * R) {
+            uint32_t ent[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int e = base + 32 * r + lane;
+                ent[r] = e < stride ? __ldg(row + e) : 0xFFFFFFFFu;
+            }
+            if (base == 0) {
+                __syncwarp();                  // every lane has read G[k*]
+                if (lane == 0) {
+                    G[kstar] = 2 * (-gv) + (xk ^ 1);   // Delta_k* -> -Delta_k*, x_k* flipped
+                    atomicOr(&dirty[(kstar >> 5) >> 5], 1u << ((kstar >> 5) & 31));   // its segment max fell
+                }
+            }
+            int g[R], delta[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) g[r] = ent[r] != 0xFFFFFFFFu ? G[ent[r] >> 8] : 0;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int q = static_cast<int>(static_cast<int8_t>(ent[r] & 0xFFu));
+                delta[r] = ent[r] != 0xFFFFFFFFu ? ((g[r] & 1) ? -d2 : d2) * q : 0;   // 2 d (1 - 2 x_j) Q_jk*
+                if (delta[r]) G[ent[r] >> 8] = g[r] + 2 * delta[r];
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!delta[r]) continue;
+                const int j = static_cast<int>(ent[r] >> 8), sg = j >> 5, lj = j & 31;
+                if (delta[r] > 0)
+                    atomicMax(&segkey[sg], seg_key(g[r] + 2 * delta[r], lj));
+                else if (segkey[sg] == seg_key(g[r], lj))
+                    atomicOr(&dirty[sg >> 5], 1u << (sg & 31));   // the segment's own max fell
             }
         }
         __syncwarp();
@@ -155,18 +171,30 @@ ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips
 int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                          int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
     if (m <= 0) return 0;
-    if (!c.csr_ptr) return 1;
+    if (!c.ell) return 1;
     const int nseg = (c.n + 31) / 32;
     const int words = nseg * 32 + nseg + (nseg + 31) / 32;
-    const size_t smem = static_cast<size_t>(kSW) * words * sizeof(int);
+    const size_t per_warp = static_cast<size_t>(words) * sizeof(int);
+    // solutions per CTA: 4 while a warp's gains are small, else 1 (finest fill of shared memory)
+    const int sw = per_warp > 16 * 1024 ? 1 : 4;
+    const size_t smem = sw * per_warp;
     if (smem > 227 * 1024) return 1;
-    cudaFuncSetAttribute(ascend_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    const unsigned grid = static_cast<unsigned>((m + kSW - 1) / kSW);
-    ascend_sparse_kernel<<<grid, 32 * kSW, smem, c.stream>>>(
-        slots_dev, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.csr_ptr, c.csr_ent, c.gains, c.f,
-        c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev), nseg, words);
-    ++c.launches;
-    return 0;
+    const unsigned grid = static_cast<unsigned>((m + sw - 1) / sw);
+    const int need = (c.ell_stride + 31) / 32;   // entries per lane for a one-pass row
+#define UBQP_SP(R)                                                                                          \
+    if (need <= R || R == 32) {                                                                             \
+        cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+                             static_cast<int>(smem));                                                       \
+        ascend_sparse_kernel<R><<<grid, 32 * sw, smem, c.stream>>>(                                         \
+            slots_dev, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.ell_stride, c.ell,  \
+            c.gains, c.f, c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev), nseg,  \
+            words);                                                                                         \
+        ++c.launches;                                                                                       \
+        return 0;                                                                                           \
+    }
+    UBQP_SP(2) UBQP_SP(4) UBQP_SP(8) UBQP_SP(16) UBQP_SP(32)
+#undef UBQP_SP
+    return 1;
 }
 
 }  // namespace ubqp

@@ -68,6 +68,32 @@ struct EvalParams {
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// Arrival on a fold counter.  The 128 epilogue threads' partial stores are ordered before the
+// counter update by the named barrier and the release (cumulative) of the atomic; the last
+// arriver's acquire fence orders its reads of the other CTAs' partials after it.  No
+// sequentially consistent fence / L1 invalidation in the hot loop (UBQP_FOLD_SYNC=1 selects
+// __threadfence() on both sides, for A/B).
+#ifndef UBQP_FOLD_SYNC
+#define UBQP_FOLD_SYNC 0
+#endif
+__device__ __forceinline__ unsigned arrive_release(unsigned *ctr) {
+#if UBQP_FOLD_SYNC == 1
+    __threadfence();
+    return atomicAdd(ctr, 1u);
+#else
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
+    return old;
+#endif
+}
+__device__ __forceinline__ void acquire_fence() {
+#if UBQP_FOLD_SYNC == 1
+    __threadfence();
+#else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ int kbs_of(int nt, int num_k_blocks, bool sym) {
     return sym ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
 }
@@ -111,13 +137,12 @@ __device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, in
                                           long long *s_red) {
     epi_bar();                                         // the 128 partials of this item are stored
     if (t == 0) {
-        __threadfence();
-        const unsigned old = atomicAdd(&p.grp_cnt[group], 1u);
+        const unsigned old = arrive_release(&p.grp_cnt[group]);
         s_flag[0] = old + 1u == static_cast<unsigned>(p.items_per_group) ? 1u : 0u;
+        if (s_flag[0]) acquire_fence();
     }
     epi_bar();
     if (!s_flag[0]) return;
-    __threadfence();
     const int64_t row = group * 128 + t;
     const bool ok = row < p.K;
     // sum the partials of every (non-empty) item of this group, plane by plane
@@ -225,14 +250,12 @@ __device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, in
     }
     // last group overall folds every group's result into the statistics
     if (t == 0) {
-        __threadfence();
-        unsigned *done = p.grp_cnt + p.num_groups;
-        const unsigned old = atomicAdd(done, 1u);
+        const unsigned old = arrive_release(p.grp_cnt + p.num_groups);
         s_flag[0] = old + 1u == static_cast<unsigned>(p.num_groups) ? 1u : 0u;
+        if (s_flag[0]) acquire_fence();
     }
     epi_bar();
     if (!s_flag[0]) return;
-    __threadfence();
     if (p.mode == kFoldInt) {
         long long S = 0, M = -1;
         for (int64_t g = t; g < p.num_groups; g += 128) {

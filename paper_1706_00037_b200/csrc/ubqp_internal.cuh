@@ -52,10 +52,11 @@ struct Ctx {
     int qmax = 0;                // max |Q_ij| of the loaded integer Q
     int8_t *Q8L = nullptr;       // [q_rows][n_pad] lower triangle of Q (row j: Q_ji for i <= j): f-only eval
     Operand op_full, op_tri;     // integer Q: Q8 (gains) and Q8L (f only)
-    // sparse rows of the integer Q (NEXT-3): CSR without the diagonal, entries (j << 8 | (q & 0xFF))
+    // sparse rows of the integer Q (NEXT-3): fixed-stride (ELL) rows without the diagonal,
+    // entries (j << 8 | (q & 0xFF)), padded with 0xFFFFFFFF to ell_stride (longest row, x32)
     int64_t nnz = 0;             // off-diagonal nonzeros
-    int32_t *csr_ptr = nullptr;  // [n + 1]
-    uint32_t *csr_ent = nullptr; // [nnz]
+    int ell_stride = 0;
+    uint32_t *ell = nullptr;     // [n][ell_stride]
     int asc_kernel = 0;          // 0 auto (by density), 1 dense, 2 sparse (UBQP_OPT_ASCENT)
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
