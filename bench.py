@@ -221,19 +221,23 @@ def run_ours(args, cfg, rank, world, local_rank):
     launches0 = u.launches
 
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clk:
         t_start.record(stream)
-        for _ in range(args.steps):
+        marks[0].record(stream)
+        for i in range(args.steps):
             m, gkey = step(True)
+            marks[i + 1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = u.launches - launches0
     ms_step = t_start.elapsed_time(t_end) / args.steps
+    step_ms = [marks[i].elapsed_time(marks[i + 1]) for i in range(args.steps)]
     eval_ms = acc["eval"] / args.steps
     asc_ms = acc["asc"] / args.steps
     t = torch.tensor([ms_step, eval_ms, asc_ms, float(flips_total), float(m)], dtype=torch.float64,
@@ -259,15 +263,17 @@ def run_ours(args, cfg, rank, world, local_rank):
     h_fl = torch.empty(max(kl, 1), dtype=torch.int32, pin_memory=True)
     h_bits = torch.empty((max(kl, 1), W), dtype=torch.int64, pin_memory=True)
     h_key = torch.empty(1, dtype=torch.int64, pin_memory=True)
-    e_steps = max(1, min(args.steps, 3))
+    e_steps = args.steps
     d_stats = ms.stats
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    emarks = [torch.cuda.Event(enable_timing=True) for _ in range(e_steps + 1)]
     h2d = d2h = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0.record(stream)
-    for _ in range(e_steps):
+    emarks[0].record(stream)
+    for ei in range(e_steps):
         u.diversify(h_seed, 0, kl, rank, world)
         u.eval_batch(UBQP_EMIT_GAINS, None, h_stats)
         if world > 1:
@@ -279,9 +285,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         u.ascend(h_surv, m_e, ms.max_flips, h_f, h_fl, h_bits, h_key)
         h2d += W * 8 + m_e * 4
         d2h += 32 + m_e * 4 + m_e * (8 + 4 + W * 8) + 8
+        emarks[ei + 1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e_steps
+    e2e_median = float(np.median([emarks[i].elapsed_time(emarks[i + 1]) for i in range(e_steps)]))
     te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -296,7 +304,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     int8_peak_burst = 2.0 * peaks["bf16_tflops"]             # guide: int8 dense = 2x bf16 nominal
     int8_peak_sust = 2.0 * peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     int8_meas = measure_int8_peak() if not args.no_int8_peak else None
-    int8_peak = int8_meas["burst_tops"] if int8_meas else int8_peak_burst
+    int8_ok = bool(int8_meas) and "burst_tops" in int8_meas
+    int8_peak = int8_meas["burst_tops"] if int8_ok else int8_peak_burst
     asc_bytes = flips_all / world * n                        # one int8 Q row per flip step
     asc_gbs = asc_bytes / (asc_ms * 1e-3) / 1e9 if asc_ms > 0 else 0.0
     traffic = {}
@@ -311,7 +320,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                  "traffic": traffic.get("eval_tc_pair_kernel", traffic.get("eval_tc_kernel")),
                  "kernel": "eval_tc_pair_kernel (+stats)", "ms": eval_ms,
                  "peak_note": ("measured cuBLASLt int8 GEMM (torch._int_mm 8192^3, best of 10) on this GPU"
-                               if int8_meas else "int8 = 2 x bf16 " + peaks["_source"]),
+                               if int8_ok else "int8 = 2 x bf16 " + peaks["_source"]),
                  "int8_measured": int8_meas,
                  "frac_of_2x_bf16_burst": eval_tops / int8_peak_burst,
                  "frac_of_2x_bf16_sustained": eval_tops / int8_peak_sust,
@@ -328,13 +337,22 @@ def run_ours(args, cfg, rank, world, local_rank):
     sm_mhz = clk.summary().get("sm_mhz") or 1965.0
     alu_peak = 148 * 4 * 16 / 1.25 * sm_mhz * 1e6
     upd = flips_all / world * n / (asc_ms * 1e-3) if asc_ms else 0.0
-    roof_asc["alu_view"] = {"bound": "alu", "achieved": upd, "peak": alu_peak, "unit": "variable updates/s",
-                            "frac": upd / alu_peak, "sm_mhz": sm_mhz,
-                            "derivation": "148 SMs x 4 SMSP x 16 ALU lanes/cycle / 1.25 ALU ops per variable"}
-    dominant = roof_asc if asc_ms >= eval_ms else roof_eval
+    roof_asc_alu = {"bound": "alu", "achieved": upd, "peak": alu_peak, "unit": "variable updates/s",
+                    "frac": upd / alu_peak, "traffic": traffic.get("ascend_kernel"), "kernel": "ascend_kernel",
+                    "ms": asc_ms, "steps_per_s": roof_asc["steps_per_s"], "sm_mhz": sm_mhz,
+                    "peak_derivation": "148 SMs x 4 SMSP x 16 ALU lanes/cycle (B300_MICROARCH pipe rates) / 1.25 "
+                                       "ALU-pipe instructions per variable update (DESIGN.md §7.4), at the sampled "
+                                       "SM clock",
+                    "algorithmic_work": "n variable updates (gain + running argmax) per flip step",
+                    "why_not_hbm": "Q (49 MB int8) is L2-resident (ncu L2 hit 99.5%); the byte view is hbm_view",
+                    "hbm_view": dict(roof_asc)}
+    roof_asc["alu_view"] = {k: v for k, v in roof_asc_alu.items() if k != "hbm_view"}
+    # the dominant kernel's roofline: the ascent against the ALU pipe (its real bound)
+    dominant = roof_asc_alu if asc_ms >= eval_ms else roof_eval
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": ms_step, "ms_per_step_median": float(np.median(step_ms)),
+        "ms_per_step_minmax": [min(step_ms), max(step_ms)], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "int8", "data": "synthetic",
         "dtype_detail": "int8 x int8 -> int32 tensor-core eval, int32 gains / int64 f in the ascent",
         "config": workload_config(cfg, world, {"dist_backend": backend if world > 1 else None}),
@@ -343,16 +361,20 @@ def run_ours(args, cfg, rank, world, local_rank):
         "eval_only_evals_per_s": K / (eval_ms * 1e-3),
         "survivors_per_step": m_all, "flip_steps_per_step": flips_all,
         "e2e": {"value": K / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d // e_steps,
-                "d2h_bytes_per_step": d2h // e_steps, "ms_per_step": e2e_ms,
+                "d2h_bytes_per_step": d2h // e_steps, "ms_per_step": e2e_ms, "ms_per_step_median": e2e_median,
+                "steps": e_steps,
                 "path": "C-ABI with pinned host buffers (seed in; stats, survivors, ascent outputs out)"},
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
     }
+    if world == 1 and not args.no_projection:
+        out["shard_projection"] = shard_projection(ms, x0_bits, f0, cfg, ms_step)
     if world == 1 and not args.no_cpu_baseline:
         # the cpu_baseline leg is the one place the main arm runs the oracle: its timing, and
         # a sampled exact parity check of the timed step's survivors
         out["cpu_baseline"] = cpu_baseline(cfg, Q)
+        out["cpu_baseline"].update(cpu_baseline_split())
         if not args.no_parity:
             out["cpu_baseline"]["parity"] = sampled_parity(cfg, Q, x0_bits, ms, m, rank, world)
     if world == 1 and not args.no_table1:
@@ -363,7 +385,137 @@ def run_ours(args, cfg, rank, world, local_rank):
         out["f_only_eval"] = f_only_eval(local_rank, cfg, Q)
         out["ascent_microbench"] = ascent_microbench(local_rank)
         out["relink_microbench"] = relink_microbench(local_rank)
+        out["sparse_ascent"] = sparse_ascent_microbench(local_rank, peaks)
     print(json.dumps(out), flush=True)
+
+
+def shard_projection(ms, x0_bits, f0, cfg, ms_step_1gpu):
+    """Multi-GPU readiness on one GPU: rank r of G holds the cyclic shard
+    g = r + i G (K_r = K / G); each shard's round (diversify -> eval + gains -> screen against the
+    GLOBAL T -> ascend) is timed on this B200 for every r, G in {2, 4, 8}.  The projected G-GPU
+    step is the slowest shard (max over r) -- a projection, not a measurement of G GPUs: the
+    three per-round collectives (~tens of microseconds over NVLink) are not included."""
+    import torch
+
+    from paper_1706_00037_b200 import UBQP_EMIT_GAINS
+    from paper_1706_00037_b200.multistart import key_f
+    u, stream, K = ms.u, ms.stream, cfg["K"]
+    # the global statistics of the batch (identical for every sharding)
+    u.diversify(x0_bits, 0, K, 0, 1)
+    u.eval_batch(0, None, ms.stats)
+    ssum, scount, skey, _ = ms.stats.tolist()
+    maxv = max(f0, key_f(skey))
+    out = {"what": "per-rank shard rounds (g = r + i G) timed one after another on one B200; the projected "
+                   "G-GPU step is the slowest shard; collectives not included", "ms_1gpu": ms_step_1gpu}
+    slots_per_wave = 148 * 6                                  # ascent CTAs resident at n = 7000
+    for G in (2, 4, 8):
+        per = []
+        surv = []
+        for r in range(G):
+            kr = len(range(r, K, G))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            u.diversify(x0_bits, 0, kr, r, G)
+            u.eval_batch(UBQP_EMIT_GAINS, None, ms.stats)
+            m, _ = u.screen(cfg["lam"], ssum, scount, maxv, ms.surv)
+            u.ascend(ms.surv, m, ms.max_flips, ms.f_asc, ms.flips, ms.bits, ms.key)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            per.append(e0.elapsed_time(e1))
+            surv.append(m)
+        mx = max(per)
+        out[f"G{G}"] = {"per_rank_ms": per, "max_ms": mx, "mean_ms": float(np.mean(per)),
+                        "imbalance": mx / float(np.mean(per)), "survivors_per_rank": surv,
+                        "ascent_waves": max(surv) / slots_per_wave,
+                        "projected_evals_per_s": K / (mx * 1e-3),
+                        "projected_speedup": ms_step_1gpu / mx}
+    return out
+
+
+def cpu_baseline_split():
+    """BASELINE.md's CPU baseline recipe: the oracle's evaluation single-threaded and on all
+    host cores at n in {2500 (density 0.1), 5000, 7000}, and its steepest ascent
+    single-threaded on 64 microbench-A starts (n = 7000, random O3 seed 5, max_flips 10 n)."""
+    import platform
+
+    import oracle
+    cores = os.cpu_count() or 1
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    res = {"nproc": cores, "cpu_model": model, "machine": platform.machine(),
+           "oracle_build": "gcc -O2 -std=c11 -ffp-contract=off -pthread (oracle/oracle.py build_oracle)",
+           "eval_single_thread": {}, "eval_all_cores": {}}
+    for n, d, sq, k1 in ((2500, 0.1, 2, 32), (5000, 1.0, 3, 8), (7000, 1.0, 4, 4)):
+        Q = generate_Q(n, d, seed=sq)
+        X = oracle.random_solutions(n, sq, max(k1, cores) * 2)
+        t = time.perf_counter()
+        oracle.eval_batch(Q, X[:k1], 1)
+        dt1 = time.perf_counter() - t
+        t = time.perf_counter()
+        oracle.eval_batch(Q, X, cores)
+        dtn = time.perf_counter() - t
+        res["eval_single_thread"][f"n{n}"] = {"evals_per_s": k1 / dt1, "sample": k1}
+        res["eval_all_cores"][f"n{n}"] = {"evals_per_s": X.shape[0] / dtn, "sample": int(X.shape[0]),
+                                          "threads": cores}
+    n = 7000
+    Q = generate_Q(n, 1.0, seed=5)
+    X = oracle.random_solutions(n, 5, 64)
+    f = oracle.eval_batch(Q, X, cores)
+    t = time.perf_counter()
+    _, _, fl = oracle.ascend(Q, X, f, 10 * n, 1)
+    dt = time.perf_counter() - t
+    res["ascent_single_thread"] = {"n": n, "starts": 64, "flip_steps": int(fl.sum()),
+                                   "steps_per_s": float(fl.sum()) / dt, "seconds": dt}
+    return res
+
+
+def sparse_ascent_microbench(device, peaks):
+    """NEXT-3: the sparse-row ascent vs the dense register ascent on Beasley-shaped Q (density
+    0.1, the b2500 shape) and n = 7000 density 0.1: 8192 random starts, full ascent
+    (identical walks).  Algorithmic bytes of the sparse kernel: 4 bytes per off-diagonal
+    nonzero of row k* per step (L2-resident rows)."""
+    import torch
+
+    from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp
+    from paper_1706_00037_b200.ubqp import ASCENT_DENSE, ASCENT_SPARSE, OPT_ASCENT, Q_NNZ
+    res = {}
+    m = 8192
+    for n, d in ((2500, 0.1), (7000, 0.1)):
+        Q = generate_Q(n, d, seed=2)
+        u = Ubqp(device, stream=torch.cuda.current_stream().cuda_stream)
+        u.load_Q(Q, m)
+        row = u.query(Q_NNZ) / n
+        u.random(5, m)
+        u.eval_batch(UBQP_EMIT_GAINS)
+        slots = torch.arange(m, dtype=torch.int32, device="cuda")
+        r = {}
+        for name, opt in (("dense", ASCENT_DENSE), ("sparse", ASCENT_SPARSE)):
+            u.set_option(OPT_ASCENT, opt)
+            fl = torch.zeros(m, dtype=torch.int32, device="cuda")
+            best = 1e9
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                u.ascend(slots, m, 10 * n, None, fl)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            steps = int(fl.sum().item())
+            r[name] = {"ms": best, "steps": steps, "steps_per_s": steps / (best * 1e-3)}
+        r["sparse"]["GB_per_s_rows"] = r["sparse"]["steps"] * row * 4 / (r["sparse"]["ms"] * 1e-3) / 1e9
+        r["sparse"]["frac_of_hbm"] = r["sparse"]["GB_per_s_rows"] / peaks["hbm_gbs"]
+        r["speedup_sparse_vs_dense"] = r["dense"]["ms"] / r["sparse"]["ms"]
+        r["row_nnz_mean"] = row
+        res[f"n{n}_d{d}"] = r
+        u.close()
+    return res
 
 
 def measure_int8_peak():
@@ -397,7 +549,7 @@ def measure_int8_peak():
         ops = 2.0 * n ** 3
         return {"burst_tops": ops / best / 1e9, "sustained_tops": ops * cnt / e0.elapsed_time(e1) / 1e9}
     except Exception as exc:                                  # keep the bench line on failure
-        return {"error": str(exc)[:200]} and None
+        return {"error": str(exc)[:200]}
 
 
 def sampled_parity(cfg, Q, x0_bits, ms, m, rank, world, samples=8):
@@ -662,6 +814,7 @@ def main():
     ap.add_argument("--no-table1", action="store_true")
     ap.add_argument("--no-int8-peak", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-projection", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: the contract requires >= 3 warm-up steps", file=sys.stderr)

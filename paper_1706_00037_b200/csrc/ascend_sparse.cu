@@ -185,6 +185,7 @@ int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t ma
     if (need <= R || R == 32) {                                                                             \
         cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
                              static_cast<int>(smem));                                                       \
+        cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 100); \
         ascend_sparse_kernel<R><<<grid, 32 * sw, smem, c.stream>>>(                                         \
             slots_dev, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.ell_stride, c.ell,  \
             c.gains, c.f, c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev), nseg,  \
