@@ -12,14 +12,16 @@
 //   warp 0      : TMA producer (128B-swizzled boxes, smem ring)
 //   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer
 //   warps 2..5  : epilogue (tcgen05.ld 32x32b, thread = row), TMEM double-buffered
+//   warp 6      : fold (arrival counters, f and statistics of finished row groups)
 // Work item = (plane, M tile, N tile, K split), plane outermost (each plane stays
 // L2-resident for its pass), N fastest (the X band in flight is shared through L2).
 //
 // f and the screening statistics are folded in-kernel (north_star: "the mean/max screening
-// reduction fused into the epilogue"): every item stores its int32 row partials, and the
-// last item to arrive for a 128-row group (an atomic counter per group) sums them into f,
-// reduces the group's {sum f, max_key}; the last group to finish reduces all groups into the
-// stats.  Counters reset themselves, so one launch per evaluation, no memset, no stats kernel.
+// reduction fused into the epilogue"): every item's epilogue stores its int32 row partials and
+// hands the item to the CTA's fold warp (an mbarrier ring); the fold warp counts the item on its
+// 128-row group's counter, and the last item of a group sums the group's partials into f and
+// its {sum f, max_key}; the last group to finish reduces all groups into the stats.  Counters
+// reset themselves: one launch per evaluation, no memset, no stats kernel.
 #include <algorithm>
 #include <climits>
 
@@ -28,7 +30,8 @@
 namespace ubqp {
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 224;                      // 7 warps: TMA, MMA, 4 epilogue, fold
+constexpr int kFoldRing = 4;                       // epilogue -> fold warp hand-off slots
 constexpr uint32_t kABytes = kBM * kBK;             // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK;             // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
@@ -65,8 +68,6 @@ struct EvalParams {
     int64_t *stats, *stats2;              // int: {sum, K, max_key, 0}; real: ubqp_stats_real words
     int rank, world, q_exp;
 };
-
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Arrival on a fold counter.  The 128 epilogue threads' partial stores are ordered before the
 // counter update by the named barrier and the release (cumulative) of the atomic; the last
@@ -130,135 +131,118 @@ __device__ __forceinline__ double i128_to_double(__int128 v) {
 }
 
 // ---------------------------------------------------------------- fold (last arriver per group)
-// Called by the 128 epilogue threads of a CTA (t = row in group) after each stored its
-// partial of one work item for rows [128 group, 128 group + 128).
+// A dedicated fold warp (warp 6) runs this for every item of its CTA, after the four epilogue
+// warps stored their partials and arrived on the item's ring barrier -- so the counter round
+// trip and the occasional fold never sit on the epilogue's critical path (the epilogue must
+// keep pace with the MMAs).  The last arriver of a 128-row group sums the group's partials
+// into f and its {sum f, max_key} (or int128 {sum f~, max f~}); the last group overall
+// reduces every group into the statistics.
+__device__ __forceinline__ void warp_i128_reduce(__int128 &sm, __int128 &mx, bool &have) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const I128 a = to_i128(sm), b = to_i128(mx);
+        const long long sh = __shfl_xor_sync(0xffffffffu, a.hi, o);
+        const unsigned long long sl = __shfl_xor_sync(0xffffffffu, a.lo, o);
+        const long long mh = __shfl_xor_sync(0xffffffffu, b.hi, o);
+        const unsigned long long ml = __shfl_xor_sync(0xffffffffu, b.lo, o);
+        const int oh = __shfl_xor_sync(0xffffffffu, have ? 1 : 0, o);
+        sm += from_i128(sh, sl);
+        const __int128 om = from_i128(mh, ml);
+        if (oh && (!have || om > mx)) mx = om;
+        have = have || oh;
+    }
+}
+
+#ifndef UBQP_FOLD_DEBUG
+#define UBQP_FOLD_DEBUG 0   // A/B only: 1 = no fold at all
+#endif
 template <bool SYM>
-__device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, int t, uint32_t *s_flag,
-                                          long long *s_red) {
-    epi_bar();                                         // the 128 partials of this item are stored
-    if (t == 0) {
+__device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int lane) {
+#if UBQP_FOLD_DEBUG == 1
+    return;
+#endif
+    unsigned last = 0;
+    if (lane == 0) {
         const unsigned old = arrive_release(&p.grp_cnt[group]);
-        s_flag[0] = old + 1u == static_cast<unsigned>(p.items_per_group) ? 1u : 0u;
-        if (s_flag[0]) acquire_fence();
+        last = old + 1u == static_cast<unsigned>(p.items_per_group) ? 1u : 0u;
+        if (last) acquire_fence();
     }
-    epi_bar();
-    if (!s_flag[0]) return;
-    const int64_t row = group * 128 + t;
-    const bool ok = row < p.K;
-    // sum the partials of every (non-empty) item of this group, plane by plane
-    __int128 acc = 0;
-    long long fsum = 0;
-    for (int pl = p.planes - 1; pl >= 0; --pl) {
-        long long s = 0;
-        for (int nt = 0; nt < p.num_n_tiles; ++nt) {
-            const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
-            for (int ks = 0; ks < p.ksplit; ++ks) {
-                if ((ks + 1) * kbs / p.ksplit == ks * kbs / p.ksplit) continue;   // empty item
-                const int64_t si = (static_cast<int64_t>(pl) * p.num_n_tiles + nt) * p.ksplit + ks;
-                s += __ldcg(p.part + si * p.part_ld + row);
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    if (lane == 0) p.grp_cnt[group] = 0u;              // self-reset for the next launch
+    // rows group*128 + lane + 32 q: the partials of every (non-empty) item, plane by plane
+    long long isum = 0, ikey = -1;
+    __int128 rsum = 0, rmax = 0;
+    bool rhave = false;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+        const int64_t row = group * 128 + q * 32 + lane;
+        __int128 acc = 0;
+        long long fsum = 0;
+        for (int pl = p.planes - 1; pl >= 0; --pl) {
+            long long sacc = 0;
+            for (int nt = 0; nt < p.num_n_tiles; ++nt) {
+                const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
+                for (int ks = 0; ks < p.ksplit; ++ks) {
+                    if ((ks + 1) * kbs / p.ksplit == ks * kbs / p.ksplit) continue;   // empty item
+                    const int64_t si = (static_cast<int64_t>(pl) * p.num_n_tiles + nt) * p.ksplit + ks;
+                    sacc += __ldcg(p.part + si * p.part_ld + row);
+                }
             }
+            acc = acc * 128 + sacc;
+            fsum = sacc;
         }
-        acc = acc * 128 + s;
-        fsum = s;
-    }
-    if (t == 0) p.grp_cnt[group] = 0u;                 // self-reset for the next launch
-    if (p.mode == kFoldPlane) {
-        if (ok) p.f[row] = fsum;
-        return;
-    }
-    // group result: int -> {sum f, max_key}; real -> {sum f~ (int128), max f~ (int128)}
-    const int lane = t & 31, w = t >> 5;
-    if (p.mode == kFoldInt) {
-        long long key = -1, sm = 0;
-        if (ok) {
+        if (row >= p.K) continue;
+        if (p.mode == kFoldPlane) {
+            p.f[row] = fsum;
+        } else if (p.mode == kFoldInt) {
             p.f[row] = fsum;
             if (p.f2) p.f2[row] = fsum;
             const long long g = static_cast<long long>(p.rank) + row * p.world;
-            key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
-                                         static_cast<unsigned long long>((1ll << 22) - 1 - g));
-            sm = fsum;
-        }
-        for (int o = 16; o > 0; o >>= 1) {
-            sm += __shfl_xor_sync(0xffffffffu, sm, o);
-            key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
-        }
-        if (lane == 0) {
-            s_red[2 * w] = sm;
-            s_red[2 * w + 1] = key;
-        }
-        epi_bar();
-        if (t == 0) {
-            long long S = 0, M = -1;
-            for (int i = 0; i < 4; ++i) {
-                S += s_red[2 * i];
-                M = max(M, s_red[2 * i + 1]);
-            }
-            p.grp_res[4 * group + 0] = S;
-            p.grp_res[4 * group + 1] = M;
-        }
-    } else {   // kFoldReal
-        __int128 sm = 0, mx = 0;
-        bool have = false;
-        if (ok) {
+            const long long key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
+                                                         static_cast<unsigned long long>((1ll << 22) - 1 - g));
+            isum += fsum;
+            ikey = max(ikey, key);
+        } else {
             const double fr = ldexp(i128_to_double(acc), -p.q_exp);
             p.fr[row] = fr;
             if (p.fr2) p.fr2[row] = fr;
-            sm = acc;
-            mx = acc;
-            have = true;
+            rsum += acc;
+            if (!rhave || acc > rmax) rmax = acc;
+            rhave = true;
         }
-        // warp reduce: sum with carries, max (invalid rows carry have = false)
+    }
+    if (p.mode == kFoldPlane) return;
+    if (p.mode == kFoldInt) {
         for (int o = 16; o > 0; o >>= 1) {
-            const I128 a = to_i128(sm), b = to_i128(mx);
-            const long long sh = __shfl_xor_sync(0xffffffffu, a.hi, o);
-            const unsigned long long sl = __shfl_xor_sync(0xffffffffu, a.lo, o);
-            const long long mh = __shfl_xor_sync(0xffffffffu, b.hi, o);
-            const unsigned long long ml = __shfl_xor_sync(0xffffffffu, b.lo, o);
-            const int oh = __shfl_xor_sync(0xffffffffu, have ? 1 : 0, o);
-            sm += from_i128(sh, sl);
-            const __int128 om = from_i128(mh, ml);
-            if (oh && (!have || om > mx)) mx = om;
-            have = have || oh;
+            isum += __shfl_xor_sync(0xffffffffu, isum, o);
+            ikey = max(ikey, __shfl_xor_sync(0xffffffffu, ikey, o));
         }
         if (lane == 0) {
-            const I128 a = to_i128(sm), b = to_i128(mx);
-            s_red[5 * w + 0] = a.hi;
-            s_red[5 * w + 1] = static_cast<long long>(a.lo);
-            s_red[5 * w + 2] = b.hi;
-            s_red[5 * w + 3] = static_cast<long long>(b.lo);
-            s_red[5 * w + 4] = have ? 1 : 0;
+            p.grp_res[4 * group + 0] = isum;
+            p.grp_res[4 * group + 1] = ikey;
         }
-        epi_bar();
-        if (t == 0) {
-            __int128 S = 0, M = 0;
-            bool H = false;
-            for (int i = 0; i < 4; ++i) {
-                S += from_i128(s_red[5 * i], static_cast<unsigned long long>(s_red[5 * i + 1]));
-                if (s_red[5 * i + 4]) {
-                    const __int128 m2 = from_i128(s_red[5 * i + 2], static_cast<unsigned long long>(s_red[5 * i + 3]));
-                    if (!H || m2 > M) M = m2;
-                    H = true;
-                }
-            }
-            if (!H) M = kI128Min;                              // no solution in this group
-            const I128 a = to_i128(S), b = to_i128(M);
+    } else {
+        warp_i128_reduce(rsum, rmax, rhave);
+        if (!rhave) rmax = kI128Min;                   // no solution in this group
+        if (lane == 0) {
+            const I128 a = to_i128(rsum), b = to_i128(rmax);
             p.grp_res[4 * group + 0] = a.hi;
             p.grp_res[4 * group + 1] = static_cast<long long>(a.lo);
             p.grp_res[4 * group + 2] = b.hi;
             p.grp_res[4 * group + 3] = static_cast<long long>(b.lo);
         }
     }
-    // last group overall folds every group's result into the statistics
-    if (t == 0) {
+    // the last group overall folds every group's result into the statistics
+    __syncwarp();
+    last = 0;
+    if (lane == 0) {
         const unsigned old = arrive_release(p.grp_cnt + p.num_groups);
-        s_flag[0] = old + 1u == static_cast<unsigned>(p.num_groups) ? 1u : 0u;
-        if (s_flag[0]) acquire_fence();
+        last = old + 1u == static_cast<unsigned>(p.num_groups) ? 1u : 0u;
+        if (last) acquire_fence();
     }
-    epi_bar();
-    if (!s_flag[0]) return;
+    if (!__shfl_sync(0xffffffffu, last, 0)) return;
     if (p.mode == kFoldInt) {
         long long S = 0, M = -1;
-        for (int64_t g = t; g < p.num_groups; g += 128) {
+        for (int64_t g = lane; g < p.num_groups; g += 32) {
             S += __ldcg(p.grp_res + 4 * g);
             M = max(M, static_cast<long long>(__ldcg(p.grp_res + 4 * g + 1)));
         }
@@ -266,19 +250,8 @@ __device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, in
             S += __shfl_xor_sync(0xffffffffu, S, o);
             M = max(M, __shfl_xor_sync(0xffffffffu, M, o));
         }
-        epi_bar();
         if (lane == 0) {
-            s_red[2 * w] = S;
-            s_red[2 * w + 1] = M;
-        }
-        epi_bar();
-        if (t == 0) {
-            long long SS = 0, MM = -1;
-            for (int i = 0; i < 4; ++i) {
-                SS += s_red[2 * i];
-                MM = max(MM, s_red[2 * i + 1]);
-            }
-            const long long out[4] = {SS, static_cast<long long>(p.K), MM, 0};
+            const long long out[4] = {S, static_cast<long long>(p.K), M, 0};
             for (int i = 0; i < 4; ++i) {
                 p.stats[i] = out[i];
                 if (p.stats2) p.stats2[i] = out[i];
@@ -286,36 +259,18 @@ __device__ __noinline__ void group_arrive(const EvalParams &p, int64_t group, in
             p.grp_cnt[p.num_groups] = 0u;
         }
     } else {
-        __int128 S = 0, M = 0;
+        __int128 S = 0, M = kI128Min;
         bool H = false;
-        for (int64_t g = t; g < p.num_groups; g += 128) {
+        for (int64_t g = lane; g < p.num_groups; g += 32) {
             S += from_i128(__ldcg(p.grp_res + 4 * g), static_cast<unsigned long long>(__ldcg(p.grp_res + 4 * g + 1)));
             const __int128 m2 =
                 from_i128(__ldcg(p.grp_res + 4 * g + 2), static_cast<unsigned long long>(__ldcg(p.grp_res + 4 * g + 3)));
             if (!H || m2 > M) M = m2;
             H = true;
         }
-        epi_bar();
-        // 128 partial results through shared memory (5 words each), thread 0 combines
-        {
+        warp_i128_reduce(S, M, H);
+        if (lane == 0) {
             const I128 a = to_i128(S), b = to_i128(M);
-            s_red[5 * t + 0] = a.hi;
-            s_red[5 * t + 1] = static_cast<long long>(a.lo);
-            s_red[5 * t + 2] = b.hi;
-            s_red[5 * t + 3] = static_cast<long long>(b.lo);
-            s_red[5 * t + 4] = H ? 1 : 0;
-        }
-        epi_bar();
-        if (t == 0) {
-            __int128 SS = 0, MM = kI128Min;
-            for (int i = 0; i < 128; ++i) {
-                SS += from_i128(s_red[5 * i], static_cast<unsigned long long>(s_red[5 * i + 1]));
-                if (s_red[5 * i + 4]) {
-                    const __int128 m2 = from_i128(s_red[5 * i + 2], static_cast<unsigned long long>(s_red[5 * i + 3]));
-                    if (m2 > MM) MM = m2;
-                }
-            }
-            const I128 a = to_i128(SS), b = to_i128(MM);
             const long long out[6] = {a.hi, static_cast<long long>(a.lo), static_cast<long long>(p.K), b.hi,
                                       static_cast<long long>(b.lo), static_cast<long long>(static_cast<unsigned>(p.q_exp))};
             for (int i = 0; i < 6; ++i) {
@@ -421,9 +376,9 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
     uint64_t *empty = full + kStages;
     uint64_t *tfull = empty + kStages;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    uint32_t *s_flag = tmem_slot + 1;
-    __shared__ long long s_red[5 * 128];
+    uint64_t *ffull = tempty + 2;             // epilogue -> fold warp (4 warp arrivals)
+    uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -437,8 +392,13 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 128);
         }
+        for (int r = 0; r < kFoldRing; ++r) {
+            mbar_init(&ffull[r], 4);
+            mbar_init(&fempty[r], 1);
+        }
         fence_mbar_init();
         tma_prefetch(&p.tmX);
+        for (int pl = 0; pl < p.planes; ++pl) tma_prefetch(&p.tmB[pl]);
     }
     if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
     tc_fence_before();
@@ -494,13 +454,27 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
                 if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
             }
         }
+    } else if (warp == 6) {
+        // ---------------- fold warp: counts each item's arrival for its group, folds the last
+        int fslot = 0;
+        uint32_t fphase = 0;
+        for (int64_t item = blockIdx.x; item < p.num_items; item += gridDim.x) {
+            const Item it = decode_item<SYM>(p, item);
+            if (it.kb0 == it.kb1) continue;
+            mbar_wait(&ffull[fslot], fphase);
+            fold_item<SYM>(p, it.mt, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&fempty[fslot]);
+            if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
+        }
     } else {
         // ---------------- epilogue: warp w may read TMEM lanes 32*(w%4) .. +31
         const int quarter = warp & 3;
         const int row_in_tile = quarter * 32 + lane;
-        const int t = threadIdx.x - 64;
         int acc = 0;
         uint32_t acc_phase = 0;
+        int fslot = 0;
+        uint32_t fphase = 0;
         for (int64_t item = blockIdx.x; item < p.num_items; item += gridDim.x) {
             const Item it = decode_item<SYM>(p, item);
             if (it.kb0 == it.kb1) continue;
@@ -513,8 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
                 row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
+            mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
             p.part[split_index(p, it) * p.part_ld + row] = partial;
-            group_arrive<SYM>(p, it.mt, t, s_flag, s_red);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ffull[fslot]);        // release: the warp's partials are stored
+            if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
     }
@@ -545,9 +522,9 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     uint64_t *empty = full + kPairStages;
     uint64_t *tfull = empty + kPairStages;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    uint32_t *s_flag = tmem_slot + 1;
-    __shared__ long long s_red[5 * 128];
+    uint64_t *ffull = tempty + 2;             // epilogue -> fold warp (4 warp arrivals)
+    uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -564,8 +541,13 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             mbar_init(&tfull[a], 1);          // multicast commit
             mbar_init(&tempty[a], 8);         // 4 epilogue warps x 2 CTAs (leader's copy is used)
         }
+        for (int r = 0; r < kFoldRing; ++r) {
+            mbar_init(&ffull[r], 4);          // this CTA's 4 epilogue warps stored their partials
+            mbar_init(&fempty[r], 1);         // this CTA's fold warp is done with the slot
+        }
         fence_mbar_init();
         tma_prefetch(&p.tmX);
+        for (int pl = 0; pl < p.planes; ++pl) tma_prefetch(&p.tmB[pl]);
     }
     if (warp == 1) tmem_alloc_cg2(tmem_slot, kTmemCols);
     tc_fence_before();
@@ -623,15 +605,29 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
                 if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
             }
         }
+    } else if (warp == 6) {
+        // ---------------- fold warp (each CTA: its own group)
+        int fslot = 0;
+        uint32_t fphase = 0;
+        for (int64_t item = cid; item < p.num_items; item += ncl) {
+            const Item it = decode_item<SYM>(p, item);
+            if (it.kb0 == it.kb1) continue;
+            mbar_wait(&ffull[fslot], fphase);
+            fold_item<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&fempty[fslot]);
+            if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
+        }
     } else {
         // ---------------- epilogue (both CTAs: their own 128 rows)
         const int quarter = warp & 3;
         const int row_in_tile = quarter * 32 + lane;
-        const int t = threadIdx.x - 64;
         const uint32_t tempty_leader0 = mapa_u32(&tempty[0], 0);
         const uint32_t tempty_leader1 = mapa_u32(&tempty[1], 0);
         int acc = 0;
         uint32_t acc_phase = 0;
+        int fslot = 0;
+        uint32_t fphase = 0;
         for (int64_t item = cid; item < p.num_items; item += ncl) {
             const Item it = decode_item<SYM>(p, item);
             if (it.kb0 == it.kb1) continue;
@@ -646,8 +642,11 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
+            mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
             p.part[split_index(p, it) * p.part_ld + row] = partial;
-            group_arrive<SYM>(p, group, t, s_flag, s_red);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ffull[fslot]);        // release: the warp's partials are stored
+            if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
     }
