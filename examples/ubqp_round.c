@@ -2,8 +2,11 @@
  * plain C through the C-ABI of include/ubqp.h (no Python, no torch): host arrays in and out.
  *
  *   gcc -std=c99 -O2 -Iinclude examples/ubqp_round.c -Lpaper_1706_00037_b200 -lubqp \
- *       -Wl,-rpath,$PWD/paper_1706_00037_b200 -o ubqp_round && ./ubqp_round [n] [K]
+ *       -Wl,-rpath,$PWD/paper_1706_00037_b200 -o ubqp_round && ./ubqp_round [n] [K] [prefix]
  *
+ * With a prefix, Q is written to prefix.Q (int32, row-major) and the round's results to
+ * prefix.out (statistics, T, then one "slot f flips" line per survivor) -- tests/test_gpu_c_abi.py
+ * checks them against the oracle.
  * Q: symmetric, coefficients uniform in [-100, 100] from a small xorshift generator (this
  * example only; the tests and bench use inputs/generate_Q). */
 #include <stdint.h>
@@ -60,6 +63,20 @@ int main(int argc, char **argv) {
     CHECK(ubqp_ascend(h, surv, m, 10 * n, f, flips, NULL, &best)); /* steepest ascent */
     int64_t total = 0;
     for (int64_t i = 0; i < m; ++i) total += flips[i];
+    if (argc > 3) {
+        char path[4096];
+        snprintf(path, sizeof path, "%s.Q", argv[3]);
+        FILE *fq = fopen(path, "wb");
+        if (!fq || fwrite(Q, sizeof(int32_t), (size_t)n * n, fq) != (size_t)n * n) { fprintf(stderr, "write %s\n", path); return 1; }
+        fclose(fq);
+        snprintf(path, sizeof path, "%s.out", argv[3]);
+        FILE *fo = fopen(path, "w");
+        if (!fo) { fprintf(stderr, "write %s\n", path); return 1; }
+        fprintf(fo, "%lld %lld %lld %.17g %lld %lld\n", (long long)st.sum, (long long)st.count, (long long)st.max_key, T,
+                (long long)m, (long long)best);
+        for (int64_t i = 0; i < m; ++i) fprintf(fo, "%d %lld %d\n", surv[i], (long long)f[i], flips[i]);
+        fclose(fo);
+    }
     printf("n=%d K=%lld mean=%.1f max=%lld T=%.1f survivors=%lld flips=%lld best f=%lld (g=%lld)\n", n,
            (long long)K, (double)st.sum / (double)st.count, (long long)maxv, T, (long long)m, (long long)total,
            best >= 0 ? (long long)((best >> 22) - ((int64_t)1 << 40)) : 0LL,

@@ -28,11 +28,14 @@
 namespace ubqp {
 namespace {
 
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;   // row padding (j = 2^24 - 1 never occurs: n <= 16384)
+
 __device__ __forceinline__ int seg_key(int g, int lane) {   // g = 2 Delta + x
     return (g >> 1) * 32 + (31 - lane);
 }
 
-// R = ELL entries per lane held in registers per pass (stride <= 32 R: one pass per step)
+// R = ELL entries per lane held in registers per pass (the least instantiated R with stride <=
+// 32 R: one pass per step; beyond 24 x 32 entries the row takes several passes)
 template <int R>
 __global__ void __launch_bounds__(128)
 ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n, int n_pad, int W64,
@@ -99,30 +102,30 @@ ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int e = base + 32 * r + lane;
-                ent[r] = e < stride ? __ldg(row + e) : 0xFFFFFFFFu;
+                ent[r] = e < stride ? __ldg(row + e) : kSentinel;
             }
             if (base == 0) {
                 __syncwarp();                  // every lane has read G[k*]
                 if (lane == 0) {
                     G[kstar] = 2 * (-gv) + (xk ^ 1);   // Delta_k* -> -Delta_k*, x_k* flipped
-                    atomicOr(&dirty[(kstar >> 5) >> 5], 1u << ((kstar >> 5) & 31));   // its segment max fell
+                    atomicOr(&dirty[kstar >> 10], 1u << ((kstar >> 5) & 31));   // its segment max fell
                 }
             }
-            int g[R], delta[R];
+            // entries are distinct columns: every gain of the pass is read, then written back
+            int g[R];
 #pragma unroll
-            for (int r = 0; r < R; ++r) g[r] = ent[r] != 0xFFFFFFFFu ? G[ent[r] >> 8] : 0;
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int q = static_cast<int>(static_cast<int8_t>(ent[r] & 0xFFu));
-                delta[r] = ent[r] != 0xFFFFFFFFu ? ((g[r] & 1) ? -d2 : d2) * q : 0;   // 2 d (1 - 2 x_j) Q_jk*
-                if (delta[r]) G[ent[r] >> 8] = g[r] + 2 * delta[r];
-            }
+            for (int r = 0; r < R; ++r) g[r] = ent[r] != kSentinel ? G[ent[r] >> 8] : 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (!delta[r]) continue;
-                const int j = static_cast<int>(ent[r] >> 8), sg = j >> 5, lj = j & 31;
-                if (delta[r] > 0)
-                    atomicMax(&segkey[sg], seg_key(g[r] + 2 * delta[r], lj));
+                if (ent[r] == kSentinel) continue;   // padding sits only at the end of a row
+                const int j = static_cast<int>(ent[r] >> 8);
+                const int q = static_cast<int>(static_cast<int8_t>(ent[r] & 0xFFu));   // != 0
+                const int delta = ((g[r] & 1) ? -d2 : d2) * q;                   // 2 d (1 - 2 x_j) Q_jk*
+                const int ng = g[r] + 2 * delta;
+                G[j] = ng;
+                const int sg = j >> 5, lj = j & 31;
+                if (delta > 0)
+                    atomicMax(&segkey[sg], seg_key(ng, lj));
                 else if (segkey[sg] == seg_key(g[r], lj))
                     atomicOr(&dirty[sg >> 5], 1u << (sg & 31));   // the segment's own max fell
             }
@@ -182,7 +185,7 @@ int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t ma
     const unsigned grid = static_cast<unsigned>((m + sw - 1) / sw);
     const int need = (c.ell_stride + 31) / 32;   // entries per lane for a one-pass row
 #define UBQP_SP(R)                                                                                          \
-    if (need <= R || R == 32) {                                                                             \
+    if (need <= R || R == 24) {                                                                             \
         cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
                              static_cast<int>(smem));                                                       \
         cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 100); \
@@ -193,7 +196,8 @@ int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t ma
         ++c.launches;                                                                                       \
         return 0;                                                                                           \
     }
-    UBQP_SP(2) UBQP_SP(4) UBQP_SP(8) UBQP_SP(16) UBQP_SP(32)
+    UBQP_SP(1) UBQP_SP(2) UBQP_SP(3) UBQP_SP(4) UBQP_SP(5) UBQP_SP(6) UBQP_SP(7) UBQP_SP(8)
+    UBQP_SP(10) UBQP_SP(12) UBQP_SP(14) UBQP_SP(16) UBQP_SP(20) UBQP_SP(24)
 #undef UBQP_SP
     return 1;
 }

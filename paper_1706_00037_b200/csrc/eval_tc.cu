@@ -81,6 +81,8 @@ __device__ __forceinline__ unsigned arrive_release(unsigned *ctr) {
 #if UBQP_FOLD_SYNC == 1
     __threadfence();
     return atomicAdd(ctr, 1u);
+#elif UBQP_FOLD_SYNC == 2
+    return atomicAdd(ctr, 1u);   // A/B only: relaxed (no ordering of the partials), measures the fence
 #else
     unsigned old;
     asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(ctr) : "memory");
@@ -156,7 +158,7 @@ __device__ __forceinline__ void warp_i128_reduce(__int128 &sm, __int128 &mx, boo
 #define UBQP_FOLD_DEBUG 0   // A/B only: 1 = no fold at all
 #endif
 template <bool SYM>
-__device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int lane) {
+__device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, int lane) {
 #if UBQP_FOLD_DEBUG == 1
     return;
 #endif
@@ -168,29 +170,52 @@ __device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int l
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     if (lane == 0) p.grp_cnt[group] = 0u;              // self-reset for the next launch
-    // rows group*128 + lane + 32 q: the partials of every (non-empty) item, plane by plane
+#if UBQP_FOLD_DEBUG == 3
+    return;                                            // A/B only: counters without the fold work
+#endif
+    // lane owns rows group*128 + 4 lane .. +3: one 16-byte load per (plane, item), all of a
+    // plane's loads independent (8 in flight), accumulated plane by plane (Horner, base 128)
     long long isum = 0, ikey = -1;
     __int128 rsum = 0, rmax = 0;
     bool rhave = false;
-#pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-        const int64_t row = group * 128 + q * 32 + lane;
-        __int128 acc = 0;
-        long long fsum = 0;
-        for (int pl = p.planes - 1; pl >= 0; --pl) {
-            long long sacc = 0;
-            for (int nt = 0; nt < p.num_n_tiles; ++nt) {
+    const int64_t row0 = group * 128 + 4 * lane;
+    __int128 acc[4] = {0, 0, 0, 0};
+    long long fs[4] = {0, 0, 0, 0};
+    const int nsplit = p.num_n_tiles * p.ksplit;
+    const int64_t ld4 = p.part_ld / 4;
+    for (int pl = p.planes - 1; pl >= 0; --pl) {
+        long long sacc[4] = {0, 0, 0, 0};
+        const int4 *base = reinterpret_cast<const int4 *>(p.part + static_cast<int64_t>(pl) * nsplit * p.part_ld + row0);
+        // batches of 8 independent loads (the slot of an empty item is never written: masked)
+        for (int s0 = 0; s0 < nsplit; s0 += 8) {
+            int4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int si = s0 + u;
+                const int nt = si / p.ksplit, ks = si - nt * p.ksplit;
                 const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
-                for (int ks = 0; ks < p.ksplit; ++ks) {
-                    if ((ks + 1) * kbs / p.ksplit == ks * kbs / p.ksplit) continue;   // empty item
-                    const int64_t si = (static_cast<int64_t>(pl) * p.num_n_tiles + nt) * p.ksplit + ks;
-                    sacc += __ldcg(p.part + si * p.part_ld + row);
-                }
+                const bool live = si < nsplit && (ks + 1) * kbs / p.ksplit != ks * kbs / p.ksplit;
+                v[u] = live ? __ldcg(base + si * ld4) : make_int4(0, 0, 0, 0);
             }
-            acc = acc * 128 + sacc;
-            fsum = sacc;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                sacc[0] += v[u].x;
+                sacc[1] += v[u].y;
+                sacc[2] += v[u].z;
+                sacc[3] += v[u].w;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            acc[q] = acc[q] * 128 + sacc[q];
+            fs[q] = sacc[q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t row = row0 + q;
         if (row >= p.K) continue;
+        const long long fsum = fs[q];
         if (p.mode == kFoldPlane) {
             p.f[row] = fsum;
         } else if (p.mode == kFoldInt) {
@@ -202,11 +227,11 @@ __device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int l
             isum += fsum;
             ikey = max(ikey, key);
         } else {
-            const double fr = ldexp(i128_to_double(acc), -p.q_exp);
+            const double fr = ldexp(i128_to_double(acc[q]), -p.q_exp);
             p.fr[row] = fr;
             if (p.fr2) p.fr2[row] = fr;
-            rsum += acc;
-            if (!rhave || acc > rmax) rmax = acc;
+            rsum += acc[q];
+            if (!rhave || acc[q] > rmax) rmax = acc[q];
             rhave = true;
         }
     }
@@ -242,6 +267,7 @@ __device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int l
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     if (p.mode == kFoldInt) {
         long long S = 0, M = -1;
+#pragma unroll 8
         for (int64_t g = lane; g < p.num_groups; g += 32) {
             S += __ldcg(p.grp_res + 4 * g);
             M = max(M, static_cast<long long>(__ldcg(p.grp_res + 4 * g + 1)));
@@ -261,6 +287,7 @@ __device__ __noinline__ void fold_item(const EvalParams &p, int64_t group, int l
     } else {
         __int128 S = 0, M = kI128Min;
         bool H = false;
+#pragma unroll 4
         for (int64_t g = lane; g < p.num_groups; g += 32) {
             S += from_i128(__ldcg(p.grp_res + 4 * g), static_cast<unsigned long long>(__ldcg(p.grp_res + 4 * g + 1)));
             const __int128 m2 =
