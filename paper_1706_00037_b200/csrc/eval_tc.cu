@@ -50,7 +50,7 @@ struct EvalParams {
     CUtensorMap tmB[kMaxPlanes];          // B per plane (256-row boxes single-CTA, 128-row pair)
     const int32_t *diag[kMaxPlanes];      // per-plane diagonal (SYM term, gains)
     int planes;
-    int n_pad, W64, num_n_tiles, num_k_blocks, ksplit;
+    int n_pad, W64, num_n_tiles, num_k_blocks, ksplit, ksplit_lg;   // ksplit = 2^ksplit_lg
     int64_t K, mn_tiles, num_items;
     const uint64_t *Xb;
     int32_t *gains;                       // EMIT_GAINS target [K][n_pad] (single plane launches)
@@ -186,19 +186,21 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
     for (int pl = p.planes - 1; pl >= 0; --pl) {
         long long sacc[4] = {0, 0, 0, 0};
         const int4 *base = reinterpret_cast<const int4 *>(p.part + static_cast<int64_t>(pl) * nsplit * p.part_ld + row0);
-        // batches of 8 independent loads (the slot of an empty item is never written: masked)
-        for (int s0 = 0; s0 < nsplit; s0 += 8) {
-            int4 v[8];
+        // batches of 16 independent loads (the slot of an empty item is never written: masked;
+        // ksplit is a power of two)
+        const int lg = p.ksplit_lg;
+        for (int s0 = 0; s0 < nsplit; s0 += 16) {
+            int4 v[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 const int si = s0 + u;
-                const int nt = si / p.ksplit, ks = si - nt * p.ksplit;
+                const int nt = si >> lg, ks = si & (p.ksplit - 1);
                 const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
-                const bool live = si < nsplit && (ks + 1) * kbs / p.ksplit != ks * kbs / p.ksplit;
+                const bool live = si < nsplit && (((ks + 1) * kbs) >> lg) != ((ks * kbs) >> lg);
                 v[u] = live ? __ldcg(base + si * ld4) : make_int4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 sacc[0] += v[u].x;
                 sacc[1] += v[u].y;
                 sacc[2] += v[u].z;
@@ -313,12 +315,29 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
 // time and folds  f_k += sum_j x_kj Y_kj  (or, triangular: x_kj (2 Y_kj - Q_jj), the Q_jj term
 // only in the K split that owns the diagonal) and, with gains, stores
 // Delta_kj = Q_jj + 2 (1 - 2 x_kj) Y_kj.  Returns the row's int32 partial of f.
+// The tile's diagonal slice (256 ints) is staged per warp in shared memory (sdiag, one
+// coalesced round trip) and the row's 256 solution bits are loaded up front: no memory
+// latency inside the TMEM drain loop (what bounds small-K launches).
 template <bool SYM>
 __device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bool row_ok, int n0, int W64,
                                                  int n_pad, const uint64_t *__restrict__ Xb,
                                                  const int32_t *__restrict__ diag, int32_t *__restrict__ gains,
-                                                 int emit_gains, bool with_diag) {
+                                                 int emit_gains, bool with_diag, int32_t *sdiag, int lane) {
     using namespace dev;
+    const bool need_diag = SYM ? with_diag : (emit_gains != 0);
+    __syncwarp();                                      // the previous tile's reads of sdiag are done
+    if (need_diag) {
+        const int4 *dg = reinterpret_cast<const int4 *>(diag + n0);
+        reinterpret_cast<int4 *>(sdiag)[lane] = __ldg(dg + lane);
+        reinterpret_cast<int4 *>(sdiag)[lane + 32] = __ldg(dg + lane + 32);
+    }
+    uint64_t xw[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int w = (n0 >> 6) + q;
+        xw[q] = (row_ok && w < W64) ? Xb[row * W64 + w] : 0ull;
+    }
+    __syncwarp();
     int32_t partial = 0;
 #pragma unroll 1
     for (int c = 0; c < kBN / 32; ++c) {
@@ -326,30 +345,34 @@ __device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bo
         tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
         tmem_wait_ld();
         const int col0 = n0 + c * 32;
-        uint32_t bits = 0;
-        if (row_ok && (col0 >> 6) < W64)
-            bits = static_cast<uint32_t>(Xb[row * W64 + (col0 >> 6)] >> (col0 & 63));
+        const int q = c >> 1;                          // select, not an indexed (local) array
+        const uint64_t wq = q == 0 ? xw[0] : (q == 1 ? xw[1] : (q == 2 ? xw[2] : xw[3]));
+        const uint32_t bits = static_cast<uint32_t>(wq >> (32 * (c & 1)));
+        const int4 *dg = reinterpret_cast<const int4 *>(sdiag + c * 32);
         if constexpr (SYM) {
-            const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
+            if (with_diag) {
 #pragma unroll
-            for (int i4 = 0; i4 < 8; ++i4) {
-                const int4 d = __ldg(dg + i4);
-                const int dd[4] = {d.x, d.y, d.z, d.w};
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const int4 d = dg[i4];
+                    const int dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int i = 4 * i4 + e;
-                    partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - (with_diag ? dd[e] : 0) : 0;
+                    for (int e = 0; e < 4; ++e) {
+                        const int i = 4 * i4 + e;
+                        partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
+                    }
                 }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) : 0;
             }
         } else {
 #pragma unroll
             for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
             if (emit_gains && row_ok && col0 < n_pad) {
-                const int4 *dg = reinterpret_cast<const int4 *>(diag + col0);
                 int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
-                    const int4 d = __ldg(dg + i4);
+                    const int4 d = dg[i4];
                     int o[4];
                     const int dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
@@ -406,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
     uint64_t *ffull = tempty + 2;             // epilogue -> fold warp (4 warp arrivals)
     uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
+    __shared__ __align__(16) int32_t s_diag[4 * kBN];   // per epilogue warp: the tile's diagonal slice
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -511,7 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
             tc_fence_after();
             const int32_t partial = epilogue_tile<SYM>(
                 tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
-                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0);
+                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0,
+                s_diag + quarter * kBN, lane);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
@@ -552,6 +577,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     uint64_t *ffull = tempty + 2;             // epilogue -> fold warp (4 warp arrivals)
     uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
+    __shared__ __align__(16) int32_t s_diag[4 * kBN];   // per epilogue warp: the tile's diagonal slice
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -665,7 +691,8 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             tc_fence_after();
             const int32_t partial = epilogue_tile<SYM>(
                 tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
-                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0);
+                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0,
+                s_diag + quarter * kBN, lane);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
@@ -733,6 +760,7 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
     p.num_n_tiles = s.num_n_tiles;
     p.num_k_blocks = s.num_k_blocks;
     p.ksplit = s.ksplit;
+    p.ksplit_lg = __builtin_ctz(static_cast<unsigned>(s.ksplit));
     p.K = L.k;
     p.mn_tiles = s.mn_tiles;
     p.num_items = s.num_items;
