@@ -275,10 +275,10 @@ enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KL
 int ubqp_query(ubqp_t h, int what, int64_t *value);
 
 /* Kernel selection (results never depend on it; every choice is exact):
- *   UBQP_OPT_ASCENT     0 = automatic (the sparse-row ascent when Q's off-diagonal density
- *                       is at most the measured crossover and its rows were built), 1 = dense
- *                       register ascent, 2 = sparse-row ascent (NEXT-3; E_STATE if the sparse
- *                       rows were not built).  Used by ubqp_ascend.
+ *   UBQP_OPT_ASCENT     0 = automatic (currently the dense register ascent at every density:
+ *                       the sparse-row kernel measured slower at densities 0.02-0.2, DESIGN.md
+ *                       §7.4'), 1 = dense register ascent, 2 = sparse-row ascent (NEXT-3;
+ *                       E_STATE if the sparse rows were not built).  Used by ubqp_ascend.
  *   UBQP_OPT_EVAL_PAIR  1 = CTA-pair (cta_group::2) evaluation (default), 0 = single CTA.
  *   UBQP_OPT_EVAL_TRI   1 = f-only evaluations use the lower triangle of Q (default), 0 = full.
  * Errors: E_INVALID (unknown option or value). */

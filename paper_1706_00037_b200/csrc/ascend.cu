@@ -483,9 +483,11 @@ static int launch_walk(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_
 }
 
 bool ascent_uses_sparse(const Ctx &c) {
+    // automatic selection: the dense register kernel everywhere -- the sparse-row kernel was
+    // measured slower at every density tried (0.02 .. 0.2, n = 1000 .. 7000; DESIGN.md §7.4')
     if (c.asc_kernel == 2) return true;
     if (c.asc_kernel == 1 || !c.ell || c.n < 2) return false;
-    return static_cast<double>(c.nnz) <= kSparseAutoDensity * c.n * (c.n - 1.0);
+    return static_cast<double>(c.nnz) < kSparseAutoDensity * c.n * (c.n - 1.0);
 }
 
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,

@@ -24,6 +24,7 @@
 // reset themselves: one launch per evaluation, no memset, no stats kernel.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "ubqp_internal.cuh"
 
@@ -725,10 +726,22 @@ EvalShape eval_shape(const Ctx &c, int64_t k, int planes, bool emit_gains, bool 
     s.num_m_tiles = (k + rows - 1) / rows;
     s.mn_tiles = s.num_m_tiles * s.num_n_tiles;
     s.ksplit = 1;
-    // f-only launches too small to fill the pairs twice split K (<= 8 ways)
-    if (s.pair && !emit_gains)
-        while (s.ksplit < 8 && s.mn_tiles * planes * s.ksplit < c.num_sms && s.num_k_blocks >= 4 * s.ksplit)
-            s.ksplit *= 2;
+    // f-only launches with fewer tiles than CTA pairs split K until every pair has one item
+    // (<= 8 ways): each extra item costs an epilogue and a fold, so splitting further loses
+    // (measured at K = 1000: n = 2500 15.9 us at 2 ways, 25.0 at 4, 48.8 at 8).  UBQP_KSPLIT
+    // forces a power of two (tuning sweeps).
+    static const int forced = [] {
+        const char *e = getenv("UBQP_KSPLIT");
+        return e ? atoi(e) : 0;
+    }();
+    if (s.pair && !emit_gains) {
+        if (forced > 0) {
+            while (s.ksplit < forced && s.ksplit < 16 && s.num_k_blocks >= 2 * s.ksplit) s.ksplit *= 2;
+        } else {
+            while (s.ksplit < 8 && s.mn_tiles * planes * s.ksplit < c.num_sms / 2 && s.num_k_blocks >= 4 * s.ksplit)
+                s.ksplit *= 2;
+        }
+    }
     s.num_items = s.mn_tiles * planes * s.ksplit;
     int nonempty = 0;
     for (int nt = 0; nt < s.num_n_tiles; ++nt) {

@@ -165,8 +165,9 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
 // ascend_sparse.cu (NEXT-3): the same walk on CSR rows; 1 if the rows were not built / too large
 int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                          int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
-// off-diagonal density at or below which UBQP_OPT_ASCENT = 0 picks the sparse kernel (measured crossover)
-constexpr double kSparseAutoDensity = 0.15;
+// off-diagonal density below which UBQP_OPT_ASCENT = 0 picks the sparse kernel: 0 = never (it
+// was measured slower than the dense kernel at every density tried, DESIGN.md §7.4')
+constexpr double kSparseAutoDensity = 0.0;
 bool ascent_uses_sparse(const Ctx &c);
 // path relinking (O11) of batch slots toward guides[i mod n_guides] on the ascent kernel
 int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
