@@ -1,9 +1,10 @@
 """Summarise ncu captures into profiles/ (committed evidence).
 
-    python tools/ncu_summary.py <round-tag> <launches.csv> <rep1.ncu-rep> [<rep2> ...]
+    python tools/ncu_summary.py <round-tag> <launches.csv | -> <rep1.ncu-rep> [<rep2> ...]
 
 Writes profiles/<tag>_summary.md (launch-list shares + per-kernel metrics and stall
-reasons) and updates profiles/traffic.json (dram bytes per launch, read by bench.py)."""
+reasons) and, when a launch list is given (a config-4 round), updates profiles/traffic.json
+(dram bytes per launch, read by bench.py)."""
 import csv
 import io
 import json
@@ -50,10 +51,23 @@ def to_bytes(val, unit):
 
 
 def main():
-    tag, launches = sys.argv[1], Path(sys.argv[2])
+    tag, launches = sys.argv[1], sys.argv[2]
     reps = [Path(p) for p in sys.argv[3:]]
     lines = [f"# ncu summary — {tag}", ""]
-    # launch list
+    if launches != "-":
+        lines += launch_list(Path(launches))
+    traffic_p = ROOT / "profiles" / "traffic.json"
+    traffic = json.loads(traffic_p.read_text()) if traffic_p.exists() else {}
+    lines += kernels_summary(reps, traffic)
+    out = ROOT / "profiles" / f"{tag}_summary.md"
+    out.write_text("\n".join(lines) + "\n")
+    if launches != "-":
+        traffic_p.write_text(json.dumps(traffic, indent=1) + "\n")
+    print(out)
+
+
+def launch_list(launches):
+    lines = []
     txt = [ln for ln in launches.read_text().splitlines() if not ln.startswith("==")]
     rows = list(csv.DictReader(io.StringIO("\n".join(txt))))
     tot = sum(float(r["Metric Value"].replace(",", "")) for r in rows)
@@ -68,8 +82,11 @@ def main():
     for name, (cnt, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"| `{name}` | {cnt} | {t / 1e3:.1f} | {100 * t / tot:.2f}% |")
     lines.append("")
-    traffic_p = ROOT / "profiles" / "traffic.json"
-    traffic = json.loads(traffic_p.read_text()) if traffic_p.exists() else {}
+    return lines
+
+
+def kernels_summary(reps, traffic):
+    lines = []
     for rep in reps:
         for k in raw(rep):
             kname = k["Kernel Name"][0]
@@ -97,10 +114,7 @@ def main():
                 rb = to_bytes(*k["dram__bytes_read.sum"])
                 wb = to_bytes(*k["dram__bytes_write.sum"])
                 traffic.setdefault("cfg4_n7000_K262144_glover", {})[short] = rb + wb
-    out = ROOT / "profiles" / f"{tag}_summary.md"
-    out.write_text("\n".join(lines) + "\n")
-    traffic_p.write_text(json.dumps(traffic, indent=1) + "\n")
-    print(out)
+    return lines
 
 
 if __name__ == "__main__":
