@@ -46,9 +46,9 @@ def load_peaks():
 
 def workload_config(cfg, world, extra=None):
     c = {"workload": cfg["name"], "n": cfg["n"], "density": cfg["density"], "seed_Q": cfg["seed_Q"],
-         "K_global": cfg["K"], "K_per_rank": len(range(0, cfg["K"], world)), "lambda": cfg.get("lam"),
+         "K_global": cfg["K"], "K_per_rank": -(-cfg["K"] // world), "lambda": cfg.get("lam"),
          "max_flips": cfg.get("max_flips"), "t0": 0, "Q_coeffs": "U{-100..100}\\{0}",
-         "parallelism": f"dp{world} (solutions sharded cyclically, Q replicated)",
+         "parallelism": f"dp{world} (solutions sharded in blocks of 2 dealt round robin, Q replicated)",
          "l2": "inputs larger than L2 (X8 1.85 GB + gains 7.4 GB per round); Q (49 MB) L2-resident by design"}
     if extra:
         c.update(extra)
@@ -368,15 +368,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
     }
-    if world == 1 and not args.no_projection:
-        out["shard_projection"] = shard_projection(ms, x0_bits, f0, cfg, ms_step)
     if world == 1 and not args.no_cpu_baseline:
         # the cpu_baseline leg is the one place the main arm runs the oracle: its timing, and
-        # a sampled exact parity check of the timed step's survivors
+        # a sampled exact parity check of the timed step's survivors (before anything else
+        # reuses the step's buffers)
+        parity = None if args.no_parity else sampled_parity(cfg, Q, x0_bits, ms, m, rank, world)
         out["cpu_baseline"] = cpu_baseline(cfg, Q)
         out["cpu_baseline"].update(cpu_baseline_split())
-        if not args.no_parity:
-            out["cpu_baseline"]["parity"] = sampled_parity(cfg, Q, x0_bits, ms, m, rank, world)
+        if parity is not None:
+            out["cpu_baseline"]["parity"] = parity
+    if world == 1 and not args.no_projection:
+        out["shard_projection"] = shard_projection(ms, x0_bits, f0, cfg, ms_step)
     if world == 1 and not args.no_table1:
         out["table1_eval_1000"] = table1_eval(local_rank)
         out["config1_round"] = config1_round(local_rank)
@@ -405,14 +407,17 @@ def shard_projection(ms, x0_bits, f0, cfg, ms_step_1gpu):
     u.eval_batch(0, None, ms.stats)
     ssum, scount, skey, _ = ms.stats.tolist()
     maxv = max(f0, key_f(skey))
-    out = {"what": "per-rank shard rounds (g = r + i G) timed one after another on one B200; the projected "
-                   "G-GPU step is the slowest shard; collectives not included", "ms_1gpu": ms_step_1gpu}
+    from paper_1706_00037_b200.ubqp import OPT_SHARD_BLOCK, shard_count
+    out = {"what": "per-rank shard rounds (O10 sharding, blocks of B consecutive g dealt round robin) timed one "
+                   "after another on one B200; the projected G-GPU step is the slowest shard; collectives not "
+                   "included", "ms_1gpu": ms_step_1gpu}
     slots_per_wave = 148 * 6                                  # ascent CTAs resident at n = 7000
-    for G in (2, 4, 8):
+    for B, G in ((1, 2), (1, 8), (2, 2), (2, 4), (2, 8)):
+        u.set_option(OPT_SHARD_BLOCK, B)
         per = []
         surv = []
         for r in range(G):
-            kr = len(range(r, K, G))
+            kr = shard_count(r, K, G, B)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record(stream)
@@ -425,11 +430,12 @@ def shard_projection(ms, x0_bits, f0, cfg, ms_step_1gpu):
             per.append(e0.elapsed_time(e1))
             surv.append(m)
         mx = max(per)
-        out[f"G{G}"] = {"per_rank_ms": per, "max_ms": mx, "mean_ms": float(np.mean(per)),
+        out[f"G{G}" + ("_cyclic" if B == 1 else "")] = {"block": B, "per_rank_ms": per, "max_ms": mx, "mean_ms": float(np.mean(per)),
                         "imbalance": mx / float(np.mean(per)), "survivors_per_rank": surv,
                         "ascent_waves": max(surv) / slots_per_wave,
                         "projected_evals_per_s": K / (mx * 1e-3),
                         "projected_speedup": ms_step_1gpu / mx}
+    u.set_option(OPT_SHARD_BLOCK, 2)
     return out
 
 

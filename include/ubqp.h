@@ -31,9 +31,14 @@
  *  - Solutions: bit j of a solution is bit (j & 63) of 64-bit word (j >> 6); a
  *    solution is W64 = ceil(n/64) words, least significant bit first.  Padding bits
  *    (j >= n) are ignored on input and written as 0.
- *  - Sharding (multi-GPU): slot i of a rank's batch is global solution
- *    g = rank + i*world; every output depends on g only, so results are identical for
- *    any world size.  K (global batch) <= 2^22.
+ *  - Sharding (multi-GPU, O10): slot i of a rank's batch is global
+ *    solution g = (rank + floor(i/B)*world)*B + (i mod B) -- blocks of B consecutive g dealt
+ *    round robin, B = ubqp_set_option(UBQP_OPT_SHARD_BLOCK), default 2 (B = 1: plain cyclic,
+ *    g = rank + i*world).  B = 2 keeps each (c = 0, c = 1) complement pair of Glover's generator
+ *    on one rank: with plain cyclic sharding and an even world every complemented solution
+ *    (almost never a survivor) lands on the odd ranks and the ascent work on the even ones.
+ *    Every output depends on g only, so results are identical for any world size and B.
+ *    K (global batch) <= 2^22.
  *  - max_key = ((f + 2^40) << 22) | (2^22 - 1 - g): int64, larger = better; MAX over
  *    keys picks the highest f, ties to the lowest g (a valid NCCL int64 MAX operand).
  *    -1 means "no solution".
@@ -106,7 +111,7 @@ int ubqp_diversify(ubqp_t h, const uint64_t *seed_bits, int64_t t0, int64_t k_lo
 
 /* Blend diversification ("Different diversification approaches based on blending
  * (or breeding) two solutions to generate new ones were implemented"; the operator is not
- * printed -- DESIGN.md reading R11b).  Slot i (g = rank + i*world, t = t0 + g, (h, q, c)
+ * printed -- DESIGN.md reading R11b).  Slot i (global index g, t = t0 + g, (h, q, c)
  * as in ubqp_diversify) takes parent p = parents[g mod n_parents]'s bits on the Glover
  * mask M(h,q) (on its complement within n bits when c = 1) and seed_bits' elsewhere:
  *   x = seed xor (mask_c and (p xor seed)).
@@ -120,7 +125,7 @@ int ubqp_blend(ubqp_t h, const uint64_t *seed_bits, const uint64_t *parents, int
 
 /* EvaluateRandomStarts' random solutions: bit j of slot i is bit
  * (j & 63) of SplitMix64-mix(seed + (g*W64 + (j>>6) + 1) * 0x9E3779B97F4A7C15),
- * g = rank + i*world.  Fills the batch with k_local solutions. */
+ * g = the global index of slot i (see Sharding).  Fills the batch with k_local solutions. */
 int ubqp_random(ubqp_t h, uint64_t seed, int64_t k_local, int32_t rank, int32_t world);
 
 /* Load caller solutions bits[k_local][W64] as the batch (rank/world set their g). */
@@ -271,7 +276,8 @@ int ubqp_sync(ubqp_t h);
  * integer Q, 1 if its sparse rows (fixed-stride ELL rows, NEXT-3) were built (off-diagonal density <= 0.25). */
 enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
        UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8,
-       UBQP_Q_EVAL_EXP = 9, UBQP_Q_EVAL_LIMBS = 10, UBQP_Q_NNZ = 11, UBQP_Q_SPARSE_ROWS = 12 };
+       UBQP_Q_EVAL_EXP = 9, UBQP_Q_EVAL_LIMBS = 10, UBQP_Q_NNZ = 11, UBQP_Q_SPARSE_ROWS = 12,
+       UBQP_Q_SHARD_BLOCK = 13 };
 int ubqp_query(ubqp_t h, int what, int64_t *value);
 
 /* Kernel selection (results never depend on it; every choice is exact):
@@ -281,8 +287,10 @@ int ubqp_query(ubqp_t h, int what, int64_t *value);
  *                       E_STATE if the sparse rows were not built).  Used by ubqp_ascend.
  *   UBQP_OPT_EVAL_PAIR  1 = CTA-pair (cta_group::2) evaluation (default), 0 = single CTA.
  *   UBQP_OPT_EVAL_TRI   1 = f-only evaluations use the lower triangle of Q (default), 0 = full.
+ *   UBQP_OPT_SHARD_BLOCK  B in [1, 4096], the sharding block (see Sharding; default 2); set it
+ *                       before generating a batch.
  * Errors: E_INVALID (unknown option or value). */
-enum { UBQP_OPT_ASCENT = 0, UBQP_OPT_EVAL_PAIR = 1, UBQP_OPT_EVAL_TRI = 2 };
+enum { UBQP_OPT_ASCENT = 0, UBQP_OPT_EVAL_PAIR = 1, UBQP_OPT_EVAL_TRI = 2, UBQP_OPT_SHARD_BLOCK = 3 };
 int ubqp_set_option(ubqp_t h, int what, int64_t value);
 
 #ifdef __cplusplus

@@ -22,7 +22,7 @@ __all__ = [
     "build_oracle", "xQx", "eval_batch", "gains", "splitmix_word", "random_solutions",
     "glover_params", "diversify", "blend", "pool_update", "max_key", "stats", "threshold", "screen", "ascend",
     "first_derivative_start", "relink", "polish", "run_rounds", "xQx_real", "eval_batch_real", "first_derivative_start_real",
-    "real_image", "ascend_real", "run_rounds_real", "gains_real", "batch_sum_exact",
+    "real_image", "ascend_real", "run_rounds_real", "gains_real", "batch_sum_exact", "global_index", "shard_count",
 ]
 
 
@@ -49,13 +49,13 @@ def _L():
         lib.oracle_gains.argtypes = [i32, P, P, P]
         lib.oracle_splitmix_word.argtypes = [u64, i64, i64, i64]
         lib.oracle_splitmix_word.restype = u64
-        lib.oracle_random.argtypes = [i32, u64, i64, i32, i32, P]
+        lib.oracle_random.argtypes = [i32, u64, i64, i32, i32, i32, P]
         lib.oracle_glover_params.argtypes = [i64, i32, P, P, P]
-        lib.oracle_diversify.argtypes = [i32, P, i64, i64, i32, i32, P]
-        lib.oracle_blend.argtypes = [i32, P, P, i64, i64, i64, i32, i32, P]
+        lib.oracle_diversify.argtypes = [i32, P, i64, i64, i32, i32, i32, P]
+        lib.oracle_blend.argtypes = [i32, P, P, i64, i64, i64, i32, i32, i32, P]
         lib.oracle_max_key.argtypes = [i64, i64]
         lib.oracle_max_key.restype = i64
-        lib.oracle_stats.argtypes = [i64, P, i32, i32, P]
+        lib.oracle_stats.argtypes = [i64, P, i32, i32, i32, P]
         lib.oracle_threshold.argtypes = [dbl, i64, i64, i64]
         lib.oracle_threshold.restype = dbl
         lib.oracle_screen.argtypes = [i64, P, dbl, P]
@@ -117,9 +117,20 @@ def splitmix_word(seed: int, g: int, W64: int, w: int) -> int:
     return int(_L().oracle_splitmix_word(seed & (2**64 - 1), g, W64, w))
 
 
-def random_solutions(n: int, seed: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+# O10 -- sharding: slot i on rank r <-> g = (r + floor(i/B) world) B + (i mod B)
+def global_index(i: int, rank: int, world: int, block: int = 1) -> int:
+    return (rank + (i // block) * world) * block + i % block
+
+
+def shard_count(rank: int, K: int, world: int, block: int = 1) -> int:
+    """number of g in [0, K) that O10 assigns to `rank`"""
+    full, rem = divmod(K, world * block)
+    return full * block + min(block, max(0, rem - rank * block))
+
+
+def random_solutions(n: int, seed: int, k_local: int, rank: int = 0, world: int = 1, block: int = 1) -> np.ndarray:
     X = np.zeros((k_local, n), dtype=np.uint8)
-    _L().oracle_random(n, seed & (2**64 - 1), k_local, rank, world, _p(X))
+    _L().oracle_random(n, seed & (2**64 - 1), k_local, rank, world, block, _p(X))
     return X
 
 
@@ -130,23 +141,23 @@ def glover_params(t: int, n: int):
     return h.value, q.value, c.value
 
 
-def diversify(seed_x, t0: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+def diversify(seed_x, t0: int, k_local: int, rank: int = 0, world: int = 1, block: int = 1) -> np.ndarray:
     seed_x = np.ascontiguousarray(seed_x, dtype=np.uint8).reshape(-1)
     n = seed_x.shape[0]
     X = np.zeros((k_local, n), dtype=np.uint8)
-    _L().oracle_diversify(n, _p(seed_x), t0, k_local, rank, world, _p(X))
+    _L().oracle_diversify(n, _p(seed_x), t0, k_local, rank, world, block, _p(X))
     return X
 
 
 # O4b -- blend of the incumbent with parent g mod P on the Glover mask (R11b)
-def blend(seed_x, parents, t0: int, k_local: int, rank: int = 0, world: int = 1) -> np.ndarray:
+def blend(seed_x, parents, t0: int, k_local: int, rank: int = 0, world: int = 1, block: int = 1) -> np.ndarray:
     seed_x = np.ascontiguousarray(seed_x, dtype=np.uint8).reshape(-1)
     n = seed_x.shape[0]
     parents = np.ascontiguousarray(parents, dtype=np.uint8).reshape(-1, n)
     if parents.shape[0] < 1:
         raise ValueError("blend needs at least one parent")
     X = np.zeros((k_local, n), dtype=np.uint8)
-    _L().oracle_blend(n, _p(seed_x), _p(parents), parents.shape[0], t0, k_local, rank, world, _p(X))
+    _L().oracle_blend(n, _p(seed_x), _p(parents), parents.shape[0], t0, k_local, rank, world, block, _p(X))
     return X
 
 
@@ -170,10 +181,10 @@ def max_key(f: int, g: int) -> int:
     return int(_L().oracle_max_key(f, g))
 
 
-def stats(f, rank: int = 0, world: int = 1) -> np.ndarray:
+def stats(f, rank: int = 0, world: int = 1, block: int = 1) -> np.ndarray:
     f = np.ascontiguousarray(f, dtype=np.int64)
     out = np.zeros(4, dtype=np.int64)
-    _L().oracle_stats(f.shape[0], _p(f), rank, world, _p(out))
+    _L().oracle_stats(f.shape[0], _p(f), rank, world, block, _p(out))
     return out
 
 
@@ -259,14 +270,14 @@ def polish(Q, elite, max_flips: int, nthreads: int = 1):
 # O8 -- batched rounds of Figure 2 (R5, R6, R13)
 def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
                world: int = 1, nthreads: int = 1, div: str = "glover", pool_cap: int = 8,
-               polish_end: bool = False, trace: list | None = None):
+               polish_end: bool = False, trace: list | None = None, block: int = 1):
     """Round 0: K random starts (O3, seed ``sample_seed``) -> pinned (mean_sum, mean_count)
     (P:55 "the mean is the average xQx value derived during sampling").  Incumbent =
     first-derivative start.  Round r >= 1: diversify from the incumbent with
     t0 = (r-1)*K (P:74 "Diversify(x, best_xQx, i, ...)"), evaluate, Max = max(incumbent,
     batch max) (R6), screen, ascend survivors, replace the incumbent iff the
     best ascended f is strictly greater, ties -> lowest g (R8, R14).
-    ``world`` shards every batch cyclically (O10); results must not depend on it.
+    ``world``/``block`` shard every batch (O10); results must not depend on them.
     ``div`` "blend": once the parent pool (pool_update) is non-empty, rounds blend the
     incumbent with pool[g mod P] (O4b) instead of O4.  ``polish_end``: after the last
     round, polish(pool + [incumbent]) (O11 + O7); a strictly better result is recorded as
@@ -280,7 +291,7 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
         return [make(r) for r in range(world)]
 
     f0 = [eval_batch(Q, Xr, nthreads) for Xr in shards(
-        lambda r: random_solutions(n, sample_seed, len(range(r, K, world)), r, world))]
+        lambda r: random_solutions(n, sample_seed, shard_count(r, K, world, block), r, world, block))]
     mean_sum = int(sum(int(fr.sum()) for fr in f0))
     mean_count = K
     inc_x = first_derivative_start(Q)
@@ -296,9 +307,9 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
         best_key, best = -1, None
         if div == "blend" and pool:
             P = np.stack(pool)
-            Xs = shards(lambda r: blend(inc_x, P, t0, len(range(r, K, world)), r, world))
+            Xs = shards(lambda r: blend(inc_x, P, t0, shard_count(r, K, world, block), r, world, block))
         else:
-            Xs = shards(lambda r: diversify(inc_x, t0, len(range(r, K, world)), r, world))
+            Xs = shards(lambda r: diversify(inc_x, t0, shard_count(r, K, world, block), r, world, block))
         fs = [eval_batch(Q, Xr, nthreads) for Xr in Xs]
         batch_max = max(int(fr.max()) for fr in fs if fr.size)
         T = threshold(lam, mean_sum, mean_count, max(inc_f, batch_max))
@@ -306,19 +317,23 @@ def run_rounds(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: 
               "max_value": max(inc_f, batch_max), "T": T, "survivors": [], "ascended": []}
         for r in range(world):
             s = screen(fs[r], T)
-            tr["survivors"] += [r + int(v) * world for v in s]
+            tr["survivors"] += [global_index(int(v), r, world, block) for v in s]
             if s.size == 0:
                 continue
             Xa, fa, _ = ascend(Q, Xs[r][s], fs[r][s], max_flips, nthreads)
             for i, slot in enumerate(s):
-                key = max_key(int(fa[i]), r + int(slot) * world)
-                tr["ascended"].append((r + int(slot) * world, int(fa[i])))
+                key = max_key(int(fa[i]), global_index(int(slot), r, world, block))
+                tr["ascended"].append((global_index(int(slot), r, world, block), int(fa[i])))
                 if key > best_key:
                     best_key, best = key, (int(fa[i]), Xa[i].copy())
         if trace is not None:
             tr["survivors"].sort()
             tr["ascended"].sort()
-            tr["f"] = [int(v) for g in range(K) for v in [fs[g % world][g // world]]]
+            fg = {}
+            for r in range(world):
+                for i, v in enumerate(fs[r]):
+                    fg[global_index(i, r, world, block)] = int(v)
+            tr["f"] = [fg[g] for g in range(K)]
             tr["best"] = None if best is None else (best[0], (1 << 22) - 1 - (best_key & ((1 << 22) - 1)),
                                                      best[1].copy())
             trace.append(tr)
@@ -425,7 +440,7 @@ def batch_sum_exact(Q, X):
 # O8 on a real Q (R20, R22): the batched rounds of run_rounds where every objective value is
 # the exactly rounded x^t Q x (O9) and each survivor's walk is O7 on the walk image Qt (O9b)
 def run_rounds_real(Q, K: int, rounds: int, lam: float, max_flips: int, sample_seed: int,
-                    world: int = 1, nthreads: int = 1):
+                    world: int = 1, nthreads: int = 1, block: int = 1):
     """Round 0: K random starts (O3); Mean = the exact rational mean of their objective values,
     rounded once to binary64 (the pinned sampling mean; R5).  Incumbent = the
     first-derivative start on the exactly rounded row sums, value O9.  Round r >= 1:
@@ -441,14 +456,14 @@ def run_rounds_real(Q, K: int, rounds: int, lam: float, max_flips: int, sample_s
     from fractions import Fraction
     total = Fraction(0)
     for r in range(world):
-        total += batch_sum_exact(Q, random_solutions(n, sample_seed, len(range(r, K, world)), r, world))
+        total += batch_sum_exact(Q, random_solutions(n, sample_seed, shard_count(r, K, world, block), r, world, block))
     mean = float(total / K)
     inc_x = first_derivative_start_real(Q)
     inc_f = xQx_real(Q, inc_x)
     traj = [(0, inc_f)]
     for rnd in range(1, rounds + 1):
         t0 = (rnd - 1) * K
-        Xs = [diversify(inc_x, t0, len(range(r, K, world)), r, world) for r in range(world)]
+        Xs = [diversify(inc_x, t0, shard_count(r, K, world, block), r, world, block) for r in range(world)]
         fs = [eval_batch_real(Q, Xr) for Xr in Xs]
         bmax = max(float(fr.max()) for fr in fs if fr.size)
         maxv = max(inc_f, bmax)
@@ -460,7 +475,7 @@ def run_rounds_real(Q, K: int, rounds: int, lam: float, max_flips: int, sample_s
                 continue
             Xa, _, _ = ascend(Qi, Xs[r][s], eval_batch(Qi, Xs[r][s], nthreads), max_flips, nthreads)
             for i, slot in enumerate(s):
-                cand = (xQx_real(Q, Xa[i]), -(r + int(slot) * world))
+                cand = (xQx_real(Q, Xa[i]), -global_index(int(slot), r, world, block))
                 if best is None or cand > best[0]:
                     best = (cand, Xa[i].copy())
         if best is not None and best[0][0] > inc_f:

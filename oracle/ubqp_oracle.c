@@ -111,12 +111,19 @@ uint64_t oracle_splitmix_word(uint64_t seed, int64_t g, int64_t W64, int64_t w)
     return z ^ (z >> 31);
 }
 
-/* slot i on rank r <-> global index g = r + i*world (O10) */
-void oracle_random(int n, uint64_t seed, int64_t k_local, int rank, int world, uint8_t *X)
+/* O10: slot i on rank r of `world` <-> global index g = (r + floor(i/B) world) B + (i mod B):
+ * blocks of B consecutive g, dealt round robin (B = 1: g = r + i world).  Every output depends
+ * on g only, so results do not depend on (world, B). */
+static int64_t global_index(int64_t i, int rank, int world, int block)
+{
+    return ((int64_t)rank + (i / block) * (int64_t)world) * block + i % block;
+}
+
+void oracle_random(int n, uint64_t seed, int64_t k_local, int rank, int world, int block, uint8_t *X)
 {
     int64_t W64 = (n + 63) / 64;
     for (int64_t i = 0; i < k_local; ++i) {
-        int64_t g = (int64_t)rank + i * (int64_t)world;
+        int64_t g = global_index(i, rank, world, block);
         for (int j = 0; j < n; ++j) {
             uint64_t word = oracle_splitmix_word(seed, g, W64, j / 64);
             X[i * n + j] = (uint8_t)((word >> (j % 64)) & 1u);
@@ -154,10 +161,10 @@ void oracle_glover_params(int64_t t, int n, int64_t *h, int64_t *q, int *c)
 }
 
 void oracle_diversify(int n, const uint8_t *seed, int64_t t0, int64_t k_local, int rank,
-                      int world, uint8_t *X)
+                      int world, int block, uint8_t *X)
 {
     for (int64_t i = 0; i < k_local; ++i) {
-        int64_t g = (int64_t)rank + i * (int64_t)world;
+        int64_t g = global_index(i, rank, world, block);
         int64_t h, q; int c;
         oracle_glover_params(t0 + g, n, &h, &q, &c);
         uint8_t *x = X + i * n;
@@ -177,10 +184,10 @@ void oracle_diversify(int n, const uint8_t *seed, int64_t t0, int64_t k_local, i
 /*     exactly O4.                                                               */
 /* ------------------------------------------------------------------------- */
 void oracle_blend(int n, const uint8_t *seed, const uint8_t *parents, int64_t n_parents, int64_t t0,
-                  int64_t k_local, int rank, int world, uint8_t *X)
+                  int64_t k_local, int rank, int world, int block, uint8_t *X)
 {
     for (int64_t i = 0; i < k_local; ++i) {
-        int64_t g = (int64_t)rank + i * (int64_t)world;
+        int64_t g = global_index(i, rank, world, block);
         const uint8_t *p = parents + (g % n_parents) * (int64_t)n;
         int64_t h, q; int c;
         oracle_glover_params(t0 + g, n, &h, &q, &c);
@@ -202,12 +209,12 @@ int64_t oracle_max_key(int64_t f, int64_t g)
     return (int64_t)(((uint64_t)(f + (1LL << 40)) << 22) | (uint64_t)((1LL << 22) - 1 - g));
 }
 
-void oracle_stats(int64_t k_local, const int64_t *f, int rank, int world, int64_t *out4)
+void oracle_stats(int64_t k_local, const int64_t *f, int rank, int world, int block, int64_t *out4)
 {
     int64_t sum = 0, best = -1;
     for (int64_t i = 0; i < k_local; ++i) {
         sum += f[i];
-        int64_t key = oracle_max_key(f[i], (int64_t)rank + i * (int64_t)world);
+        int64_t key = oracle_max_key(f[i], global_index(i, rank, world, block));
         if (key > best) best = key;
     }
     out4[0] = sum; out4[1] = k_local; out4[2] = best; out4[3] = 0;

@@ -311,6 +311,7 @@ int run_eval(ubqp_t h, bool emit_gains, int64_t *f_dev = nullptr, int64_t *stats
         L.stats2 = stats_dev;
         L.rank = h->rank;
         L.world = h->world;
+        L.shard_b = h->shard_b;
         const int rc = eval_launch(h, L);
         if (rc) return rc;
     }
@@ -323,7 +324,7 @@ int check_batch_args(ubqp_t h, int64_t k_local, int32_t rank, int32_t world) {
     if (h->n <= 0) return fail(h, UBQP_E_STATE, "ubqp: no Q loaded");
     if (k_local < 0 || k_local > h->k_max) return fail(h, UBQP_E_INVALID, "ubqp: k_local out of [0, k_max]");
     if (world < 1 || rank < 0 || rank >= world) return fail(h, UBQP_E_INVALID, "ubqp: bad rank/world");
-    if (k_local > 0 && static_cast<int64_t>(rank) + (k_local - 1) * world >= (1ll << 22))
+    if (k_local > 0 && ubqp::global_index(k_local - 1, rank, world, h->shard_b) >= (1ll << 22))
         return fail(h, UBQP_E_INVALID, "ubqp: global index g exceeds 2^22");
     return UBQP_OK;
 }
@@ -1006,6 +1007,7 @@ int ubqp_eval_batch_real(ubqp_t h, double *f_out, ubqp_stats_real *stats_out) {
         L.stats2 = s_dev ? reinterpret_cast<int64_t *>(stats_out) : nullptr;
         L.rank = h->rank;
         L.world = h->world;
+        L.shard_b = h->shard_b;
         L.q_exp = h->w_exp;
         const int rc = eval_launch(h, L);
         if (rc) return rc;
@@ -1074,6 +1076,7 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
         case UBQP_Q_EVAL_LIMBS: *value = h->real ? h->w_limbs : 1; break;
         case UBQP_Q_NNZ: *value = h->nnz; break;
         case UBQP_Q_SPARSE_ROWS: *value = h->ell ? 1 : 0; break;
+        case UBQP_Q_SHARD_BLOCK: *value = h->shard_b; break;
         default: return UBQP_E_INVALID;
     }
     return UBQP_OK;
@@ -1089,6 +1092,10 @@ int ubqp_set_option(ubqp_t h, int what, int64_t value) {
         case UBQP_OPT_EVAL_PAIR:
             if (value != 0 && value != 1) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_EVAL_PAIR must be 0 or 1");
             h->eval_pair = value == 1;
+            break;
+        case UBQP_OPT_SHARD_BLOCK:
+            if (value < 1 || value > 4096) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_SHARD_BLOCK must be in [1, 4096]");
+            h->shard_b = static_cast<int>(value);
             break;
         case UBQP_OPT_EVAL_TRI:
             if (value != 0 && value != 1) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_EVAL_TRI must be 0 or 1");

@@ -121,7 +121,7 @@ struct RelinkArgs {
 template <int BLOCK, int NCH, int MINB, bool FULL, bool RELINK>
 __global__ void __launch_bounds__(BLOCK, MINB)
 ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int q_ld, int W64,
-              int64_t k_local, int rank, int world, const int8_t *__restrict__ Q8,
+              int64_t k_local, int rank, int world, int shard_b, const int8_t *__restrict__ Q8,
               const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
               const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out,
               int32_t *__restrict__ flips_out, uint64_t *__restrict__ bits_out,
@@ -346,7 +346,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
             if (rl.sbest) rl.sbest[i] = best_s;
             if (rl.len) rl.len[i] = nd;
             if (best_key && best_s >= 0) {
-                const int64_t g = static_cast<int64_t>(rank) + s * world;
+                const int64_t g = global_index(s, rank, world, shard_b);
                 const long long key = static_cast<long long>(
                     (static_cast<uint64_t>(best_f + (1ll << 40)) << 22) |
                     static_cast<uint64_t>((1ll << 22) - 1 - g));
@@ -375,7 +375,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         if (f_out) f_out[i] = fv;
         if (flips_out) flips_out[i] = flips;
         if (best_key) {
-            const int64_t g = static_cast<int64_t>(rank) + s * world;
+            const int64_t g = global_index(s, rank, world, shard_b);
             const long long key = static_cast<long long>(
                 (static_cast<uint64_t>(fv + (1ll << 40)) << 22) |
                 static_cast<uint64_t>((1ll << 22) - 1 - g));
@@ -402,21 +402,21 @@ void launch_inst(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int
         const size_t seq = static_cast<size_t>(c.n_pad) * sizeof(uint16_t);
         if (full)
             ascend_kernel<BLOCK, NCH, kMinBlocks, true, true><<<grid, BLOCK, seq, c.stream>>>(
-                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.shard_b, c.Q8, c.gains, c.f,
                 c.Xb, f_dev, flips_dev, bits_dev, bk, *rl);
         else
             ascend_kernel<BLOCK, NCH, kMinBlocks, false, true><<<grid, BLOCK, seq, c.stream>>>(
-                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+                slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.shard_b, c.Q8, c.gains, c.f,
                 c.Xb, f_dev, flips_dev, bits_dev, bk, *rl);
         return;
     }
     if (full)
         ascend_kernel<BLOCK, NCH, kMinBlocks, true, false><<<grid, BLOCK, 0, c.stream>>>(
-            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.shard_b, c.Q8, c.gains, c.f,
             c.Xb, f_dev, flips_dev, bits_dev, bk, RelinkArgs{});
     else
         ascend_kernel<BLOCK, NCH, kMinBlocks, false, false><<<grid, BLOCK, 0, c.stream>>>(
-            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.Q8, c.gains, c.f,
+            slots, max_flips, c.n, c.n_pad, c.q_ld, c.W64, c.k_local, c.rank, c.world, c.shard_b, c.Q8, c.gains, c.f,
             c.Xb, f_dev, flips_dev, bits_dev, bk, RelinkArgs{});
 }
 

@@ -39,7 +39,8 @@ __device__ __forceinline__ int seg_key(int g, int lane) {   // g = 2 Delta + x
 template <int R>
 __global__ void __launch_bounds__(128)
 ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips, int n, int n_pad, int W64,
-                     int64_t k_local, int rank, int world, int stride, const uint32_t *__restrict__ ell,
+                     int64_t k_local, int rank, int world, int shard_b, int stride,
+                     const uint32_t *__restrict__ ell,
                      const int32_t *__restrict__ gains, const int64_t *__restrict__ f_in,
                      const uint64_t *__restrict__ Xb, int64_t *__restrict__ f_out, int32_t *__restrict__ flips_out,
                      uint64_t *__restrict__ bits_out, long long *__restrict__ best_key, int nseg,
@@ -161,7 +162,7 @@ ascend_sparse_kernel(const int32_t *__restrict__ slots, int64_t m, int max_flips
         if (f_out) f_out[i] = fv;
         if (flips_out) flips_out[i] = flips;
         if (best_key) {
-            const int64_t g = static_cast<int64_t>(rank) + s * world;
+            const int64_t g = global_index(s, rank, world, shard_b);
             const long long key = static_cast<long long>((static_cast<uint64_t>(fv + (1ll << 40)) << 22) |
                                                          static_cast<uint64_t>((1ll << 22) - 1 - g));
             atomicMax(best_key, key);
@@ -190,7 +191,7 @@ int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t ma
                              static_cast<int>(smem));                                                       \
         cudaFuncSetAttribute(ascend_sparse_kernel<R>, cudaFuncAttributePreferredSharedMemoryCarveout, 100); \
         ascend_sparse_kernel<R><<<grid, 32 * sw, smem, c.stream>>>(                                         \
-            slots_dev, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.ell_stride, c.ell,  \
+            slots_dev, m, max_flips, c.n, c.n_pad, c.W64, c.k_local, c.rank, c.world, c.shard_b, c.ell_stride, c.ell,  \
             c.gains, c.f, c.Xb, f_dev, flips_dev, bits_dev, reinterpret_cast<long long *>(best_dev), nseg,  \
             words);                                                                                         \
         ++c.launches;                                                                                       \

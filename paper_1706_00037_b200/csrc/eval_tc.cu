@@ -67,7 +67,7 @@ struct EvalParams {
     int64_t *f, *f2;                      // int f (kFoldInt, kFoldPlane); f2 optional second copy
     double *fr, *fr2;                     // real f (kFoldReal)
     int64_t *stats, *stats2;              // int: {sum, K, max_key, 0}; real: ubqp_stats_real words
-    int rank, world, q_exp;
+    int rank, world, shard_b, q_exp;
 };
 
 // Arrival on a fold counter.  The 128 epilogue threads' partial stores are ordered before the
@@ -224,7 +224,7 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
         } else if (p.mode == kFoldInt) {
             p.f[row] = fsum;
             if (p.f2) p.f2[row] = fsum;
-            const long long g = static_cast<long long>(p.rank) + row * p.world;
+            const long long g = global_index(row, p.rank, p.world, p.shard_b);
             const long long key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
                                                          static_cast<unsigned long long>((1ll << 22) - 1 - g));
             isum += fsum;
@@ -795,6 +795,7 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
     p.stats2 = L.stats2;
     p.rank = L.rank;
     p.world = L.world;
+    p.shard_b = L.shard_b;
     p.q_exp = L.q_exp;
     if (s.pair) {
         if (!c.eval_pair_attr_set) {   // per handle (= per device): the attribute is per device context

@@ -49,7 +49,7 @@ __device__ __forceinline__ int64_t isqrt_dev(int64_t v) {
 __global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict__ seed,
                                                      const uint64_t *__restrict__ parents,
                                                      int64_t n_parents, int64_t t0,
-                                                     int64_t k, int rank, int world, int n,
+                                                     int64_t k, int rank, int world, int B, int n,
                                                      int W64, int NW, int n_pad,
                                                      uint64_t *__restrict__ Xb,
                                                      int8_t *__restrict__ X8) {
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) glover_kernel(const uint64_t *__restrict_
     const int w = static_cast<int>(idx - slot * NW);
     uint64_t word = 0;
     if (w < W64) {
-        const int64_t g = static_cast<int64_t>(rank) + slot * world;
+        const int64_t g = global_index(slot, rank, world, B);
         const int64_t period = static_cast<int64_t>(n) * (n + 1);
         int64_t t = (t0 + g) % period;
         if (t < 0) t += period;
@@ -88,7 +88,7 @@ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void __launch_bounds__(256) random_kernel(uint64_t seed, int64_t k, int rank, int world,
+__global__ void __launch_bounds__(256) random_kernel(uint64_t seed, int64_t k, int rank, int world, int B,
                                                      int n, int W64, int NW, int n_pad,
                                                      uint64_t *__restrict__ Xb,
                                                      int8_t *__restrict__ X8) {
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) random_kernel(uint64_t seed, int64_t k, i
     const int w = static_cast<int>(idx - slot * NW);
     uint64_t word = 0;
     if (w < W64) {
-        const uint64_t g = static_cast<uint64_t>(rank) + static_cast<uint64_t>(slot) * world;
+        const uint64_t g = static_cast<uint64_t>(global_index(slot, rank, world, B));
         const uint64_t ctr = g * static_cast<uint64_t>(W64) + static_cast<uint64_t>(w) + 1ull;
         word = splitmix_mix(seed + ctr * 0x9E3779B97F4A7C15ull) & tail_mask(n, w);
         Xb[slot * W64 + w] = word;
@@ -177,7 +177,7 @@ void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k, cons
     if (k <= 0) return;
     const int NW = c.n_pad / 64;
     glover_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed_dev, parents_dev, n_parents, t0, k, c.rank,
-                                                            c.world, c.n,
+                                                            c.world, c.shard_b, c.n,
                                                             c.W64, NW, c.n_pad, c.Xb, c.X8);
     ++c.launches;
 }
@@ -185,7 +185,7 @@ void launch_glover(Ctx &c, const uint64_t *seed_dev, int64_t t0, int64_t k, cons
 void launch_random(Ctx &c, uint64_t seed, int64_t k) {
     if (k <= 0) return;
     const int NW = c.n_pad / 64;
-    random_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed, k, c.rank, c.world, c.n, c.W64,
+    random_kernel<<<blocks_for(k * NW), 256, 0, c.stream>>>(seed, k, c.rank, c.world, c.shard_b, c.n, c.W64,
                                                             NW, c.n_pad, c.Xb, c.X8);
     ++c.launches;
 }

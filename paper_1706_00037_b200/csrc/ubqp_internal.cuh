@@ -66,6 +66,7 @@ struct Ctx {
     // batch workspace
     int64_t k_max = 0, k_cap_pad = 0, k_local = -1;
     int rank = 0, world = 1;
+    int shard_b = 2;             // O10 block size B (UBQP_OPT_SHARD_BLOCK): g = (rank + (i/B) world) B + i%B
     uint64_t *Xb = nullptr;      // [k_max][W64] packed solutions
     int8_t *X8 = nullptr;        // [k_cap_pad][n_pad] expanded 0/1 bytes (GEMM A operand)
     int64_t *f = nullptr;        // [k_max] xQx of the batch
@@ -119,6 +120,12 @@ struct Ctx {
 
 constexpr int64_t kReevalRows = 8192;   // rows per re-evaluation chunk of ascend_real
 
+// O10: slot i of rank r holds global solution g = (r + floor(i/B) world) B + (i mod B),
+// blocks of B consecutive g dealt round robin; B = 1 is plain cyclic sharding.
+__host__ __device__ __forceinline__ int64_t global_index(int64_t slot, int rank, int world, int B) {
+    return (static_cast<int64_t>(rank) + (slot / B) * world) * B + slot % B;
+}
+
 // Shape of one evaluation launch (eval_tc.cu)
 struct EvalShape {
     bool pair;
@@ -135,7 +142,7 @@ struct EvalLaunch {
     int64_t *f = nullptr, *f2 = nullptr;
     double *fr = nullptr, *fr2 = nullptr;
     int64_t *stats = nullptr, *stats2 = nullptr;
-    int rank = 0, world = 1, q_exp = 0;
+    int rank = 0, world = 1, shard_b = 1, q_exp = 0;
 };
 
 // ------------------------------------------------------------------ launchers (host)

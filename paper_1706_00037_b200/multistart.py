@@ -6,7 +6,8 @@ torch.distributed (NCCL) for the only exchange steps of the method (SURVEY.md §
     the Mean and Max over all solutions), and
   * the best-record key (MAX) plus a broadcast of the winner's bits from its owner rank
     (UpdateBestAndT, P:79-80).
-Solutions are sharded cyclically (slot i on rank r <-> g = r + i*world) and Q is
+Solutions are sharded in blocks of B = 2 dealt round robin (slot i on rank r <->
+g = (r + floor(i/2) world) 2 + i mod 2, include/ubqp.h "Sharding") and Q is
 replicated; every other step runs in the kernels behind include/ubqp.h.
 """
 from __future__ import annotations
@@ -17,7 +18,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .ubqp import UBQP_EMIT_GAINS, Ubqp
+from .ubqp import (OPT_SHARD_BLOCK, SHARD_BLOCK_DEFAULT, UBQP_EMIT_GAINS, Ubqp, global_index, shard_count,
+                   shard_owner)
 
 KEY_SHIFT = 22
 F_OFFSET = 1 << 40
@@ -62,10 +64,10 @@ def combine_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
     return stats
 
 
-def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None):
+def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None, block: int = SHARD_BLOCK_DEFAULT):
     """key int64[1] (rank-local best max_key, -1 = none), bits_row int64[W64] (that
     solution's bits on its rank).  Returns (global key, winner bits) on every rank: MAX of
-    the keys, then a broadcast of the bits from the rank owning g = key_g (g mod world)."""
+    the keys, then a broadcast of the bits from the rank owning g = key_g (O10 sharding)."""
     rank, world = dist_info(group)
     if world == 1:
         return int(key.item()), bits_row
@@ -74,7 +76,7 @@ def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None):
     k = int(gk.item())
     if k < 0:
         return k, bits_row
-    owner = key_g(k) % world
+    owner = shard_owner(key_g(k), world, block)[0]
     out = bits_row.clone()
     src = dist.get_global_rank(group, owner) if group is not None else owner
     dist.broadcast(out, src=src, group=group)
@@ -114,7 +116,8 @@ class MultiStart:
         self.device = torch.cuda.current_device() if device is None else device
         self.n = int(Q.shape[0])
         self.K = int(K)
-        self.k_local = len(range(self.rank, self.K, self.world))
+        self.block = SHARD_BLOCK_DEFAULT
+        self.k_local = shard_count(self.rank, self.K, self.world, self.block)
         self.lam = float(lam)
         self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
         self.qmax = int(np.abs(np.asarray(Q)).max()) if self.n else 0
@@ -122,6 +125,7 @@ class MultiStart:
         self.stream = torch.cuda.Stream(device=self.device)
         torch.cuda.set_stream(self.stream)
         self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
+        self.u.set_option(OPT_SHARD_BLOCK, self.block)
         # workspace also holds a polish batch: all ordered pairs of <= 9 elite solutions
         self.u.load_Q(np.ascontiguousarray(Q, dtype=np.int32), max(self.k_local, POLISH_MAX_PAIRS))
         self.W64 = self.u.W64
@@ -146,7 +150,7 @@ class MultiStart:
     # EvaluateRandomStarts: (sum, count) of K random solutions
     def sample_mean(self, seed: int, K: int | None = None):
         K = self.K if K is None else K
-        kl = len(range(self.rank, K, self.world))
+        kl = shard_count(self.rank, K, self.world, self.block)
         self.u.random(seed, kl, self.rank, self.world)
         self.u.eval_batch(0, None, self.stats)
         combine_stats(self.stats, self.group)
@@ -173,12 +177,12 @@ class MultiStart:
         row = self.bits[0]
         if m > 0 and self.world > 1:
             k_local = int(self.key.item())
-            if k_local >= 0 and key_g(k_local) % self.world == self.rank:
-                slot = (key_g(k_local) - self.rank) // self.world
+            owner, slot = shard_owner(key_g(k_local), self.world, self.block) if k_local >= 0 else (-1, -1)
+            if k_local >= 0 and owner == self.rank:
                 i = int(torch.searchsorted(self.surv[:m], torch.tensor([slot], dtype=torch.int32,
                                                                         device=self.surv.device)).item())
                 row = self.bits[i]
-        best_key, best_bits = combine_best(self.key, row.contiguous(), self.group)
+        best_key, best_bits = combine_best(self.key, row.contiguous(), self.group, self.block)
         if self.world == 1 and m > 0:
             best_key = int(self.key.item())
             slot = key_g(best_key)
@@ -302,12 +306,14 @@ class MultiStartReal:
         self.device = torch.cuda.current_device() if device is None else device
         self.n = int(Q.shape[0])
         self.K = int(K)
-        self.k_local = len(range(self.rank, self.K, self.world))
+        self.block = SHARD_BLOCK_DEFAULT
+        self.k_local = shard_count(self.rank, self.K, self.world, self.block)
         self.lam = float(lam)
         self.max_flips = 10 * self.n if max_flips is None else int(max_flips)
         self.stream = torch.cuda.Stream(device=self.device)
         torch.cuda.set_stream(self.stream)
         self.u = Ubqp(self.device, stream=self.stream.cuda_stream)
+        self.u.set_option(OPT_SHARD_BLOCK, self.block)
         self.u.load_Q_real(np.ascontiguousarray(Q), max(self.k_local, 1))
         self.e = self.u.real_exp          # walk image (R20)
         self.w = self.u.eval_exp          # evaluation image (R22)
@@ -353,7 +359,7 @@ class MultiStartReal:
             fa = self.fa[:m]
             mx = float(fa.max().item())
             i = int(torch.nonzero(fa == mx)[0].item())      # lowest slot = lowest g among ties
-            best = (mx, self.rank + int(self.surv[i].item()) * self.world, i)
+            best = (mx, global_index(int(self.surv[i].item()), self.rank, self.world, self.block), i)
         # global best: highest f, then lowest g; the owner broadcasts the bits
         cand = torch.tensor([best[0], float(best[1])] if best else [float("-inf"), float(2**62)], dtype=torch.float64)
         if self.world > 1:
@@ -368,7 +374,7 @@ class MultiStartReal:
         if gf == float("-inf"):
             return m, T, None, None
         gg = int(gg)
-        owner = gg % self.world
+        owner = shard_owner(gg, self.world, self.block)[0]
         row = self.bits[best[2]].clone() if (best and owner == self.rank) else torch.zeros_like(self.bits[0])
         if self.world > 1:
             src = dist.get_global_rank(self.group, owner) if self.group is not None else owner

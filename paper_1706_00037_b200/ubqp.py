@@ -28,8 +28,27 @@ EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ub
            "ubqp_load_Q_real", "ubqp_eval_batch_real", "ubqp_screen_real", "ubqp_ascend_real",
            "ubqp_set_option"]
 UBQP_F32, UBQP_F64 = 1, 2
-Q_REAL_EXP, Q_IS_REAL, Q_EVAL_EXP, Q_EVAL_LIMBS, Q_NNZ, Q_SPARSE_ROWS = 7, 8, 9, 10, 11, 12
-OPT_ASCENT, OPT_EVAL_PAIR, OPT_EVAL_TRI = 0, 1, 2
+Q_REAL_EXP, Q_IS_REAL, Q_EVAL_EXP, Q_EVAL_LIMBS, Q_NNZ, Q_SPARSE_ROWS, Q_SHARD_BLOCK = 7, 8, 9, 10, 11, 12, 13
+OPT_ASCENT, OPT_EVAL_PAIR, OPT_EVAL_TRI, OPT_SHARD_BLOCK = 0, 1, 2, 3
+SHARD_BLOCK_DEFAULT = 2
+
+
+def global_index(i: int, rank: int, world: int, block: int = SHARD_BLOCK_DEFAULT) -> int:
+    """global solution index of slot i on rank `rank` (include/ubqp.h "Sharding")"""
+    return (rank + (i // block) * world) * block + i % block
+
+
+def shard_count(rank: int, K: int, world: int, block: int = SHARD_BLOCK_DEFAULT) -> int:
+    """slots of `rank` in a global batch of K"""
+    full, rem = divmod(K, world * block)
+    return full * block + min(block, max(0, rem - rank * block))
+
+
+def shard_owner(g: int, world: int, block: int = SHARD_BLOCK_DEFAULT):
+    """(rank, slot) holding global solution g"""
+    b, o = divmod(g, block)
+    r, q = b % world, b // world
+    return r, q * block + o
 ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE = 0, 1, 2
 
 
@@ -227,6 +246,10 @@ class Ubqp:
     def eval_exp(self) -> int:
         """exponent w of the evaluation image (R22)"""
         return self.query(Q_EVAL_EXP)
+
+    @property
+    def shard_block(self) -> int:
+        return self.query(Q_SHARD_BLOCK)
 
     @property
     def eval_limbs(self) -> int:

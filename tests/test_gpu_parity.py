@@ -80,10 +80,10 @@ def test_blend_batch_bits(n):
         pd = torch.from_numpy(pb.view(np.int64)).cuda()
         for world in (1, 3):
             for r in range(world):
-                kl = len(range(r, K, world))
+                kl = oracle.shard_count(r, K, world, 2)          # the library's default block B = 2
                 u.blend(pack_bits(seed_x)[0], pd, P, 9, kl, r, world)
                 torch.cuda.synchronize()
-                assert np.array_equal(_batch(u, kl, n), oracle.blend(seed_x, parents, 9, kl, r, world)), (P, r)
+                assert np.array_equal(_batch(u, kl, n), oracle.blend(seed_x, parents, 9, kl, r, world, 2)), (P, r)
 
 
 def test_blend_complement_parent_equals_glover_and_errors():
@@ -219,24 +219,35 @@ def test_ascend_computes_missing_gains_and_empty():
     assert key[0] == -1
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharding_matches_single_rank(world):
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("block", [1, 2, 5])
+def test_sharding_matches_single_rank(world, block):
+    """O10: rank r holds g = (r + floor(i/B) world) B + (i mod B); every rank's f and stats
+    come from the global batch, and they partition it"""
+    from paper_1706_00037_b200.ubqp import OPT_SHARD_BLOCK, Q_SHARD_BLOCK
     n, K = 400, 1000
     Q = generate_Q(n, 0.5, seed=5)
     seed_x = np.random.default_rng(1).integers(0, 2, size=n).astype(np.uint8)
     full = oracle.eval_batch(Q, oracle.diversify(seed_x, 3, K), nthreads=8)
     u = _handle_with(Q, K)
+    assert u.query(Q_SHARD_BLOCK) == 2
+    u.set_option(OPT_SHARD_BLOCK, block)
     tot = 0
     best = -1
+    seen = []
     for r in range(world):
-        kr = len(range(r, K, world))
+        kr = oracle.shard_count(r, K, world, block)
+        gs = [oracle.global_index(i, r, world, block) for i in range(kr)]
+        seen += gs
         u.diversify(pack_bits(seed_x)[0], 3, kr, r, world)
         f = np.zeros(kr, np.int64)
         st = ubqp_stats()
         u.eval_batch(0, f, st)
-        assert np.array_equal(f, full[r::world])
+        assert np.array_equal(f, full[gs])
+        assert st.max_key == oracle.stats(full[gs], r, world, block)[2]
         tot += st.sum
         best = max(best, st.max_key)
+    assert sorted(seen) == list(range(K))
     ost = oracle.stats(full)
     assert tot == ost[0] and best == ost[2]
 

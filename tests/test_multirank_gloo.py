@@ -1,6 +1,6 @@
 """World-size-2 (and 3) CPU tests of the multi-GPU exchange steps (gloo backend).
 
-Each rank computes its cyclic shard (slot i <-> g = rank + i*world) with the
+Each rank computes its shard (slot i <-> g = (rank + floor(i/2) world) 2 + i mod 2) with the
 oracle, then the product's exchange code (paper_1706_00037_b200.multistart.combine_stats /
 combine_best, the only collectives of the method) must reproduce the single-rank oracle
 result exactly: global sum/count/max_key and the best ascended solution with its bits.
@@ -35,10 +35,11 @@ def _worker(rank, world, port, n, K, lam, max_flips, out):
         Q = generate_Q(n, 0.5, seed=42)
         x0 = oracle.first_derivative_start(Q)
         f0 = oracle.xQx(Q, x0)
-        kl = len(range(rank, K, world))
-        X = oracle.diversify(x0, 0, kl, rank, world)
+        B = 2                                        # the library's default sharding block (O10)
+        kl = oracle.shard_count(rank, K, world, B)
+        X = oracle.diversify(x0, 0, kl, rank, world, B)
         f = oracle.eval_batch(Q, X)
-        st = torch.from_numpy(oracle.stats(f, rank, world))
+        st = torch.from_numpy(oracle.stats(f, rank, world, B))
         combine_stats(st)
         ssum, scount, skey, _ = st.tolist()
         T = oracle.threshold(lam, ssum, scount, max(f0, key_f(skey)))
@@ -47,7 +48,7 @@ def _worker(rank, world, port, n, K, lam, max_flips, out):
         row = np.zeros(len(pack_bits(x0)[0]), dtype=np.int64)
         if s.size:
             Xa, fa, _ = oracle.ascend(Q, X[s], f[s], max_flips)
-            keys = [oracle.max_key(int(fa[i]), rank + int(s[i]) * world) for i in range(s.size)]
+            keys = [oracle.max_key(int(fa[i]), oracle.global_index(int(s[i]), rank, world, B)) for i in range(s.size)]
             b = int(np.argmax(keys))
             key = keys[b]
             row = pack_bits(Xa[b])[0].view(np.int64)

@@ -132,6 +132,29 @@ def test_random_sharding_is_cyclic():
             assert np.array_equal(part, full[r::world])
 
 
+def test_block_sharding_partitions_the_batch():
+    """O10 with block B: rank r holds g = (r + floor(i/B) world) B + (i mod B); written out by
+    hand for K = 11, world = 3, B = 2: rank 0 -> 0 1 6 7, rank 1 -> 2 3 8 9, rank 2 -> 4 5 10"""
+    want = {0: [0, 1, 6, 7], 1: [2, 3, 8, 9], 2: [4, 5, 10]}
+    for r, gs in want.items():
+        assert oracle.shard_count(r, 11, 3, 2) == len(gs)
+        assert [oracle.global_index(i, r, 3, 2) for i in range(len(gs))] == gs
+    n = 50
+    full = oracle.random_solutions(n, 4, 101)
+    seed = np.random.default_rng(2).integers(0, 2, size=n).astype(np.uint8)
+    dfull = oracle.diversify(seed, 7, 101)
+    for world in (1, 2, 3, 8):
+        for B in (1, 2, 3, 16):
+            seen = []
+            for r in range(world):
+                k = oracle.shard_count(r, 101, world, B)
+                gs = [oracle.global_index(i, r, world, B) for i in range(k)]
+                seen += gs
+                assert np.array_equal(oracle.random_solutions(n, 4, k, r, world, B), full[gs])
+                assert np.array_equal(oracle.diversify(seed, 7, k, r, world, B), dfull[gs])
+            assert sorted(seen) == list(range(101))
+
+
 def test_sampled_mean_matches_expectation():
     """E f = sum_i Q_ii/2 + sum_{i!=j} Q_ij/4 under iid Bernoulli(1/2) bits."""
     hits = 0
