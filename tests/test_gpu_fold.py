@@ -1,0 +1,75 @@
+"""The in-kernel fold of the evaluation (eval_tc.cu: per-item partials, per-group counters, a
+fold warp, self-resetting counters): randomised shapes, both kernels (CTA pair / single CTA),
+triangular and full GEMMs, K splits, ranks and shard blocks, and back-to-back launches that
+reuse the counters -- f and the statistics must equal the oracle exactly every time."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from inputs import generate_Q
+
+torch = pytest.importorskip("torch")
+hyp = pytest.importorskip("hypothesis")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp, ubqp_stats  # noqa: E402
+from paper_1706_00037_b200.build import build_lib  # noqa: E402
+from paper_1706_00037_b200.ubqp import OPT_EVAL_PAIR, OPT_EVAL_TRI, OPT_SHARD_BLOCK  # noqa: E402
+
+build_lib()
+
+
+@settings(max_examples=int(os.environ.get("UBQP_HYPO_EXAMPLES", 60)), deadline=None)
+@given(n=st.integers(1, 1300), K=st.integers(1, 1500), pair=st.booleans(), tri=st.booleans(),
+       world=st.integers(1, 5), block=st.integers(1, 4), seed=st.integers(0, 2**31 - 1))
+def test_fold_matches_oracle(n, K, pair, tri, world, block, seed):
+    Q = generate_Q(n, 0.6, seed=seed)
+    rank = seed % world
+    kl = oracle.shard_count(rank, K, world, block)
+    u = Ubqp(0)
+    u.set_option(OPT_EVAL_PAIR, int(pair))
+    u.set_option(OPT_EVAL_TRI, int(tri))
+    u.set_option(OPT_SHARD_BLOCK, block)
+    u.load_Q(Q, max(kl, 1))
+    u.random(seed, kl, rank, world)
+    X = oracle.random_solutions(n, seed, kl, rank, world, block)
+    fo = oracle.eval_batch(Q, X, nthreads=8)
+    so = oracle.stats(fo, rank, world, block)
+    for flags in (0, UBQP_EMIT_GAINS, 0):            # back to back: the counters reset themselves
+        f = np.zeros(max(kl, 1), np.int64)
+        stt = ubqp_stats()
+        u.eval_batch(flags, f, stt)
+        assert np.array_equal(f[:kl], fo)
+        assert (stt.sum, stt.count, stt.max_key) == (int(so[0]), kl, int(so[2]) if kl else -1)
+
+
+def test_fold_device_outputs_and_interleaved_handles():
+    """device f / stats are written by the kernel; two handles on one stream interleave"""
+    n1, n2, K = 700, 333, 2000
+    Q1, Q2 = generate_Q(n1, 1.0, seed=1), generate_Q(n2, 0.2, seed=2)
+    s = torch.cuda.Stream()
+    u1 = Ubqp(0, stream=s.cuda_stream)
+    u2 = Ubqp(0, stream=s.cuda_stream)
+    u1.load_Q(Q1, K)
+    u2.load_Q(Q2, K)
+    u1.random(3, K)
+    u2.random(4, K)
+    f1 = torch.zeros(K, dtype=torch.int64, device="cuda")
+    f2 = torch.zeros(K, dtype=torch.int64, device="cuda")
+    s1 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    s2 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        u1.eval_batch(0, f1, s1)
+        u2.eval_batch(UBQP_EMIT_GAINS, f2, s2)
+    torch.cuda.synchronize()
+    fo1 = oracle.eval_batch(Q1, oracle.random_solutions(n1, 3, K), nthreads=8)
+    fo2 = oracle.eval_batch(Q2, oracle.random_solutions(n2, 4, K), nthreads=8)
+    assert np.array_equal(f1.cpu().numpy(), fo1) and np.array_equal(f2.cpu().numpy(), fo2)
+    assert s1.cpu().tolist()[:3] == oracle.stats(fo1).tolist()[:3]
+    assert s2.cpu().tolist()[:3] == oracle.stats(fo2).tolist()[:3]
