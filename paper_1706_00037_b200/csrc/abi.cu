@@ -1077,6 +1077,7 @@ int ubqp_query(ubqp_t h, int what, int64_t *value) {
         case UBQP_Q_NNZ: *value = h->nnz; break;
         case UBQP_Q_SPARSE_ROWS: *value = h->ell ? 1 : 0; break;
         case UBQP_Q_SHARD_BLOCK: *value = h->shard_b; break;
+        case UBQP_Q_ASCENT_LAST: *value = h->asc_last; break;
         default: return UBQP_E_INVALID;
     }
     return UBQP_OK;
@@ -1086,7 +1087,7 @@ int ubqp_set_option(ubqp_t h, int what, int64_t value) {
     GUARD(h);
     switch (what) {
         case UBQP_OPT_ASCENT:
-            if (value < 0 || value > 2) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_ASCENT must be 0, 1 or 2");
+            if (value < 0 || value > 3) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_ASCENT must be 0, 1, 2 or 3");
             h->asc_kernel = static_cast<int>(value);
             break;
         case UBQP_OPT_EVAL_PAIR:

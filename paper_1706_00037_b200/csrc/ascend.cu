@@ -492,8 +492,16 @@ bool ascent_uses_sparse(const Ctx &c) {
 
 int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                   int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev) {
-    if (ascent_uses_sparse(c))
+    if (ascent_uses_sparse(c)) {
+        c.asc_last = 2;
         return launch_ascend_sparse(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);
+    }
+    // automatic: the warp-per-solution kernel where it measured faster (n_pad in (4096, 7168])
+    if (c.asc_kernel == 3 || (c.asc_kernel == 0 && c.n_pad > 4096 && c.n_pad <= ascend_warp_max_n())) {
+        c.asc_last = 3;
+        return launch_ascend_warp(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);
+    }
+    c.asc_last = 1;
     return launch_walk(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev, nullptr);
 }
 

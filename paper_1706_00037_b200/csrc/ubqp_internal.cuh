@@ -57,7 +57,8 @@ struct Ctx {
     int64_t nnz = 0;             // off-diagonal nonzeros
     int ell_stride = 0;
     uint32_t *ell = nullptr;     // [n][ell_stride]
-    int asc_kernel = 0;          // 0 auto (by density), 1 dense, 2 sparse (UBQP_OPT_ASCENT)
+    int asc_kernel = 0;          // 0 auto, 1 dense CTA, 2 sparse, 3 dense warp (UBQP_OPT_ASCENT)
+    int asc_last = 0;            // kernel of the last ascend (1 CTA, 2 sparse, 3 warp; UBQP_Q_ASCENT_LAST)
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
     int64_t parents_cap = 0;
@@ -176,6 +177,10 @@ int launch_ascend_sparse(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t ma
 // was measured slower than the dense kernel at every density tried, DESIGN.md §7.4')
 constexpr double kSparseAutoDensity = 0.0;
 bool ascent_uses_sparse(const Ctx &c);
+// ascend_warp.cu: one warp per solution (n_pad <= ascend_warp_max_n()); 1 if n is out of range
+int ascend_warp_max_n();
+int launch_ascend_warp(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
+                       int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
 // path relinking (O11) of batch slots toward guides[i mod n_guides] on the ascent kernel
 int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
                   int64_t *f_dev, int32_t *steps_dev, int32_t *sbest_dev, int32_t *len_dev, uint64_t *bits_dev,

@@ -29,6 +29,7 @@ EXPORTS = ["ubqp_version", "ubqp_create", "ubqp_destroy", "ubqp_last_error", "ub
            "ubqp_set_option"]
 UBQP_F32, UBQP_F64 = 1, 2
 Q_REAL_EXP, Q_IS_REAL, Q_EVAL_EXP, Q_EVAL_LIMBS, Q_NNZ, Q_SPARSE_ROWS, Q_SHARD_BLOCK = 7, 8, 9, 10, 11, 12, 13
+Q_ASCENT_LAST = 14
 OPT_ASCENT, OPT_EVAL_PAIR, OPT_EVAL_TRI, OPT_SHARD_BLOCK = 0, 1, 2, 3
 SHARD_BLOCK_DEFAULT = 2
 
@@ -49,7 +50,7 @@ def shard_owner(g: int, world: int, block: int = SHARD_BLOCK_DEFAULT):
     b, o = divmod(g, block)
     r, q = b % world, b // world
     return r, q * block + o
-ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE = 0, 1, 2
+ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE, ASCENT_WARP = 0, 1, 2, 3
 
 
 class UbqpError(RuntimeError):

@@ -19,6 +19,7 @@ if not torch.cuda.is_available():
 
 from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp, UbqpError, ubqp_stats  # noqa: E402
 from paper_1706_00037_b200.build import build_lib  # noqa: E402
+from paper_1706_00037_b200.ubqp import ASCENT_AUTO, ASCENT_DENSE, ASCENT_WARP, OPT_ASCENT  # noqa: E402
 
 build_lib()
 
@@ -181,10 +182,12 @@ def test_screen_boundary_equal_fails():
 
 @pytest.mark.parametrize("n", [1, 2, 3, 50, 129, 500, 1100, 2500])
 @pytest.mark.parametrize("max_flips", [0, 3, 100000])
-def test_ascend(n, max_flips):
+@pytest.mark.parametrize("kernel", [ASCENT_AUTO, ASCENT_DENSE, ASCENT_WARP])
+def test_ascend(n, max_flips, kernel):
     Q = generate_Q(n, 0.8, seed=31 + n)
     K = 64 if n >= 1100 else 200
     u = _handle_with(Q, K)
+    u.set_option(OPT_ASCENT, kernel)
     u.random(17, K)
     u.eval_batch(UBQP_EMIT_GAINS)
     slots = np.arange(0, K, 3, dtype=np.int32)[::-1].copy()   # unordered subset
@@ -345,12 +348,15 @@ def test_full_size_sampled(n, K, kind):
 
 
 @pytest.mark.parametrize("n", [5000, 7000, 9000, 12000])
-def test_ascend_full_size(n):
-    """Default shapes 64x5 (n=5000), 64x7 (n=7000), 96x6 (n=9000), 128x6 (n=12000), exact
-    against the oracle."""
+@pytest.mark.parametrize("kernel", [ASCENT_AUTO, ASCENT_DENSE])
+def test_ascend_full_size(n, kernel):
+    """Automatic kernel (warp per solution up to n_pad = 7168, CTA above) and the CTA
+    kernel's default shapes 64x5 (n=5000), 64x7 (n=7000), 96x6 (n=9000), 128x6 (n=12000),
+    exact against the oracle."""
     Q = generate_Q(n, 1.0, seed=4)
     K = 24
     u = _handle_with(Q, K)
+    u.set_option(OPT_ASCENT, kernel)
     b = np.zeros(u.W64, np.uint64)
     u.first_derivative(b)
     x0 = unpack_bits(b, n)[0]
@@ -372,6 +378,7 @@ def test_ascend_forced_shapes(shape, monkeypatch):
     n, K = 2500, 40
     Q = generate_Q(n, 0.5, seed=8)
     u = _handle_with(Q, K)
+    u.set_option(OPT_ASCENT, ASCENT_DENSE)       # the shapes of the CTA kernel
     u.random(9, K)
     u.eval_batch(UBQP_EMIT_GAINS)
     monkeypatch.setenv("UBQP_ASC_CFG", shape)

@@ -1,6 +1,8 @@
 """SURVEY §8(d) ascent microbench A at n in {2500, 5000, 7000} (8192 random starts, full
-ascent): flip steps/s per n on the library UBQP_LIB points at (A/B of kernel variants).
+ascent): flip steps/s per n and per dense kernel (1 = CTA, 3 = warp per solution; UBQP_ASC_KERNELS
+="1,3"), on the library UBQP_LIB points at (A/B of kernel variants).
     python tools/asc_micro.py [n ...]"""
+import os
 import sys
 from pathlib import Path
 
@@ -10,6 +12,7 @@ import torch  # noqa: E402
 
 from inputs import generate_Q  # noqa: E402
 from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp  # noqa: E402
+from paper_1706_00037_b200.ubqp import OPT_ASCENT  # noqa: E402
 
 
 def main():
@@ -26,16 +29,21 @@ def main():
         slots = torch.arange(m, dtype=torch.int32, device="cuda")
         flips = torch.zeros(m, dtype=torch.int32, device="cuda")
         fo = torch.zeros(m, dtype=torch.int64, device="cuda")
-        best = 1e9
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            u.ascend(slots, m, 10 * n, fo, flips)
-            e1.record()
-            torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1))
-        steps = int(flips.sum().item())
-        print(f"n={n}: {best:7.2f} ms  {steps / best / 1e6:6.3f} Gsteps/s  fsum={int(fo.sum().item())}", flush=True)
+        for kern in [int(k) for k in os.environ.get("UBQP_ASC_KERNELS", "1,3").split(",")]:
+            if kern == 3 and n > 7168:
+                continue
+            u.set_option(OPT_ASCENT, kern)
+            best = 1e9
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                u.ascend(slots, m, 10 * n, fo, flips)
+                e1.record()
+                torch.cuda.synchronize()
+                best = min(best, e0.elapsed_time(e1))
+            steps = int(flips.sum().item())
+            print(f"n={n} kernel={kern}: {best:7.2f} ms  {steps / best / 1e6:6.3f} Gsteps/s  steps={steps} "
+                  f"fsum={int(fo.sum().item())}", flush=True)
         u.close()
 
 

@@ -26,6 +26,7 @@ METRICS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active", "FMA-heavy pipe %"),
     ("sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active", "tensor IMMA pipe %"),
     ("sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active", "TC pipe %"),
     ("launch__registers_per_thread", "registers/thread"),
