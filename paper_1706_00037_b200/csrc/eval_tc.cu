@@ -33,6 +33,10 @@ namespace {
 
 constexpr int kThreads = 224;                      // 7 warps: TMA, MMA, 4 epilogue, fold
 constexpr int kFoldRing = 4;                       // epilogue -> fold warp hand-off slots
+#ifndef UBQP_FOLD_BATCH
+#define UBQP_FOLD_BATCH 32
+#endif
+constexpr int kFoldBatch = UBQP_FOLD_BATCH;        // partial loads in flight per fold lane
 constexpr uint32_t kABytes = kBM * kBK;             // 16 KB
 constexpr uint32_t kBBytes = kBN * kBK;             // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes; // 48 KB
@@ -51,13 +55,15 @@ struct EvalParams {
     CUtensorMap tmB[kMaxPlanes];          // B per plane (256-row boxes single-CTA, 128-row pair)
     const int32_t *diag[kMaxPlanes];      // per-plane diagonal (SYM term, gains)
     int planes;
-    int n_pad, W64, num_n_tiles, num_k_blocks, ksplit, ksplit_lg;   // ksplit = 2^ksplit_lg
-    int64_t K, mn_tiles, num_items;
+    int n_pad, W64, num_n_tiles, num_k_blocks;
+    int nsplit;                           // items per (M tile, plane) = split_tab entries
+    uint32_t split_tab[kMaxSplits];       // entry o: N tile | kb0 << 8 | kb1 << 16 (host, eval_shape)
+    int64_t K, num_m_tiles, num_items;
     const uint64_t *Xb;
     int32_t *gains;                       // EMIT_GAINS target [K][n_pad] (single plane launches)
     int emit_gains;
     // fold
-    int32_t *part;                        // [planes][num_n_tiles][ksplit][part_ld] int32 row partials
+    int32_t *part;                        // [planes][nsplit][part_ld] int32 row partials
     int64_t part_ld;
     unsigned *grp_cnt;                    // [num_groups] arrival counters, then [num_groups]: done
     int items_per_group;
@@ -98,9 +104,6 @@ __device__ __forceinline__ void acquire_fence() {
 #endif
 }
 
-__device__ __forceinline__ int kbs_of(int nt, int num_k_blocks, bool sym) {
-    return sym ? min(num_k_blocks, (nt + 1) * (kBN / kBK)) : num_k_blocks;
-}
 
 // int128 helpers (hi signed, lo unsigned)
 constexpr __int128 kI128Min = static_cast<__int128>(static_cast<unsigned __int128>(1) << 127);
@@ -133,6 +136,21 @@ __device__ __forceinline__ double i128_to_double(__int128 v) {
     return neg ? -d : d;
 }
 
+#ifndef UBQP_EVAL_TRACE
+#define UBQP_EVAL_TRACE 0      // 1: %globaltimer stamps per CTA at the pipeline's milestones (debug)
+#endif
+#if UBQP_EVAL_TRACE
+__device__ unsigned long long g_evtrace[512][16];
+__device__ __forceinline__ void ev_stamp(int slot) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 512) g_evtrace[blockIdx.x][slot] = t;
+}
+#define EV_STAMP(s) ev_stamp(s)
+#else
+#define EV_STAMP(s) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- fold (last arriver per group)
 // A dedicated fold warp (warp 6) runs this for every item of its CTA, after the four epilogue
 // warps stored their partials and arrived on the item's ring barrier -- so the counter round
@@ -159,7 +177,7 @@ __device__ __forceinline__ void warp_i128_reduce(__int128 &sm, __int128 &mx, boo
 #define UBQP_FOLD_DEBUG 0   // A/B only: 1 = no fold at all
 #endif
 template <bool SYM>
-__device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, int lane) {
+__device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, int lane, int4 *sfold) {
 #if UBQP_FOLD_DEBUG == 1
     return;
 #endif
@@ -169,7 +187,9 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
         last = old + 1u == static_cast<unsigned>(p.items_per_group) ? 1u : 0u;
         if (last) acquire_fence();
     }
+    if (lane == 0) EV_STAMP(10);
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
+    if (lane == 0) EV_STAMP(14);
     if (lane == 0) p.grp_cnt[group] = 0u;              // self-reset for the next launch
 #if UBQP_FOLD_DEBUG == 3
     return;                                            // A/B only: counters without the fold work
@@ -182,32 +202,34 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
     const int64_t row0 = group * 128 + 4 * lane;
     __int128 acc[4] = {0, 0, 0, 0};
     long long fs[4] = {0, 0, 0, 0};
-    const int nsplit = p.num_n_tiles * p.ksplit;
+    const int nsplit = p.nsplit;
     const int64_t ld4 = p.part_ld / 4;
     for (int pl = p.planes - 1; pl >= 0; --pl) {
         long long sacc[4] = {0, 0, 0, 0};
         const int4 *base = reinterpret_cast<const int4 *>(p.part + static_cast<int64_t>(pl) * nsplit * p.part_ld + row0);
-        // batches of 16 independent loads (the slot of an empty item is never written: masked;
-        // ksplit is a power of two)
-        const int lg = p.ksplit_lg;
-        for (int s0 = 0; s0 < nsplit; s0 += 16) {
-            int4 v[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int si = s0 + u;
-                const int nt = si >> lg, ks = si & (p.ksplit - 1);
-                const int kbs = kbs_of(nt, p.num_k_blocks, SYM);
-                const bool live = si < nsplit && (((ks + 1) * kbs) >> lg) != ((ks * kbs) >> lg);
-                v[u] = live ? __ldcg(base + si * ld4) : make_int4(0, 0, 0, 0);
+        // batches of 32 independent loads: one round trip for up to 32 partials per row (every
+        // split-table entry owns >= 1 K block, so every slot is written)
+        for (int s0 = 0; s0 < nsplit; s0 += kFoldBatch) {
+            // every lane copies its own 16-byte pieces into shared memory (LDGSTS: no registers,
+            // so all of them are in flight at once -- register loads let ptxas interleave the sums
+            // and serialise the round trips), waits for its own group and reads them back
+            const int4 *ptr = base + static_cast<int64_t>(s0) * ld4;
+            const uint32_t sdst = dev::smem_u32(sfold) + 16u * lane;
+            const int nb = min(kFoldBatch, nsplit - s0);
+            for (int u = 0; u < nb; ++u) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 512u * u), "l"(ptr) : "memory");
+                ptr += ld4;
             }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                sacc[0] += v[u].x;
-                sacc[1] += v[u].y;
-                sacc[2] += v[u].z;
-                sacc[3] += v[u].w;
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+            for (int u = 0; u < nb; ++u) {             // shared-memory latency only
+                const int4 t = sfold[32 * u + lane];
+                sacc[0] += t.x;
+                sacc[1] += t.y;
+                sacc[2] += t.z;
+                sacc[3] += t.w;
             }
         }
+        if (lane == 0) EV_STAMP(15);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             acc[q] = acc[q] * 128 + sacc[q];
@@ -224,7 +246,9 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
         } else if (p.mode == kFoldInt) {
             p.f[row] = fsum;
             if (p.f2) p.f2[row] = fsum;
-            const long long g = global_index(row, p.rank, p.world, p.shard_b);
+            const unsigned r32 = static_cast<unsigned>(row), b32 = static_cast<unsigned>(p.shard_b);
+            const long long g = p.world == 1 ? static_cast<long long>(row)     // 32-bit form of global_index
+                                             : (static_cast<long long>(p.rank) + (r32 / b32) * static_cast<long long>(p.world)) * b32 + r32 % b32;
             const long long key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
                                                          static_cast<unsigned long long>((1ll << 22) - 1 - g));
             isum += fsum;
@@ -238,6 +262,7 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
             rhave = true;
         }
     }
+    if (lane == 0) EV_STAMP(11);
     if (p.mode == kFoldPlane) return;
     if (p.mode == kFoldInt) {
         for (int o = 16; o > 0; o >>= 1) {
@@ -266,6 +291,7 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
         const unsigned old = arrive_release(p.grp_cnt + p.num_groups);
         last = old + 1u == static_cast<unsigned>(p.num_groups) ? 1u : 0u;
         if (last) acquire_fence();
+        EV_STAMP(12);
     }
     if (!__shfl_sync(0xffffffffu, last, 0)) return;
     if (p.mode == kFoldInt) {
@@ -280,6 +306,7 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
             M = max(M, __shfl_xor_sync(0xffffffffu, M, o));
         }
         if (lane == 0) {
+            EV_STAMP(13);
             const long long out[4] = {S, static_cast<long long>(p.K), M, 0};
             for (int i = 0; i < 4; ++i) {
                 p.stats[i] = out[i];
@@ -319,12 +346,14 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
 // The tile's diagonal slice (256 ints) is staged per warp in shared memory (sdiag, one
 // coalesced round trip) and the row's 256 solution bits are loaded up front: no memory
 // latency inside the TMEM drain loop (what bounds small-K launches).
+// Stage the tile's diagonal slice and load the row's 256 solution bits: independent of the
+// MMAs, so it is issued BEFORE the wait for the accumulator (measured at K = 1000: the loads'
+// round trip otherwise sits between TMEM-full and the drain).
 template <bool SYM>
-__device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bool row_ok, int n0, int W64,
-                                                 int n_pad, const uint64_t *__restrict__ Xb,
-                                                 const int32_t *__restrict__ diag, int32_t *__restrict__ gains,
-                                                 int emit_gains, bool with_diag, int32_t *sdiag, int lane) {
-    using namespace dev;
+__device__ __forceinline__ void epilogue_stage(int64_t row, bool row_ok, int n0, int W64,
+                                               const uint64_t *__restrict__ Xb, const int32_t *__restrict__ diag,
+                                               int emit_gains, bool with_diag, int32_t *sdiag, int lane,
+                                               uint64_t (&xw)[4]) {
     const bool need_diag = SYM ? with_diag : (emit_gains != 0);
     __syncwarp();                                      // the previous tile's reads of sdiag are done
     if (need_diag) {
@@ -332,86 +361,107 @@ __device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bo
         reinterpret_cast<int4 *>(sdiag)[lane] = __ldg(dg + lane);
         reinterpret_cast<int4 *>(sdiag)[lane + 32] = __ldg(dg + lane + 32);
     }
-    uint64_t xw[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int w = (n0 >> 6) + q;
         xw[q] = (row_ok && w < W64) ? Xb[row * W64 + w] : 0ull;
     }
     __syncwarp();
-    int32_t partial = 0;
-#pragma unroll 1
-    for (int c = 0; c < kBN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(c * 32), v);
-        tmem_wait_ld();
-        const int col0 = n0 + c * 32;
-        const int q = c >> 1;                          // select, not an indexed (local) array
-        const uint64_t wq = q == 0 ? xw[0] : (q == 1 ? xw[1] : (q == 2 ? xw[2] : xw[3]));
-        const uint32_t bits = static_cast<uint32_t>(wq >> (32 * (c & 1)));
-        const int4 *dg = reinterpret_cast<const int4 *>(sdiag + c * 32);
-        if constexpr (SYM) {
-            if (with_diag) {
+}
+
+// One 32-column chunk of the drain (thread = row): f partial, and with gains the gain stores.
+template <bool SYM>
+__device__ __forceinline__ void epilogue_chunk(const uint32_t (&v)[32], int c, int32_t &partial, int64_t row,
+                                               bool row_ok, int n0, int n_pad, int32_t *__restrict__ gains,
+                                               int emit_gains, bool with_diag, const int32_t *sdiag,
+                                               const uint64_t (&xw)[4]) {
+    const int col0 = n0 + c * 32;
+    const int q = c >> 1;                          // select, not an indexed (local) array
+    const uint64_t wq = q == 0 ? xw[0] : (q == 1 ? xw[1] : (q == 2 ? xw[2] : xw[3]));
+    const uint32_t bits = static_cast<uint32_t>(wq >> (32 * (c & 1)));
+    const int4 *dg = reinterpret_cast<const int4 *>(sdiag + c * 32);
+    if constexpr (SYM) {
+        if (with_diag) {
 #pragma unroll
-                for (int i4 = 0; i4 < 8; ++i4) {
-                    const int4 d = dg[i4];
-                    const int dd[4] = {d.x, d.y, d.z, d.w};
+            for (int i4 = 0; i4 < 8; ++i4) {
+                const int4 d = dg[i4];
+                const int dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int i = 4 * i4 + e;
-                        partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
-                    }
+                for (int e = 0; e < 4; ++e) {
+                    const int i = 4 * i4 + e;
+                    partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) - dd[e] : 0;
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) : 0;
             }
         } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
-            if (emit_gains && row_ok && col0 < n_pad) {
-                int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
+            for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? 2 * static_cast<int32_t>(v[i]) : 0;
+        }
+    } else {
 #pragma unroll
-                for (int i4 = 0; i4 < 8; ++i4) {
-                    const int4 d = dg[i4];
-                    int o[4];
-                    const int dd[4] = {d.x, d.y, d.z, d.w};
+        for (int i = 0; i < 32; ++i) partial += ((bits >> i) & 1u) ? static_cast<int32_t>(v[i]) : 0;
+        if (emit_gains && row_ok && col0 < n_pad) {
+            int4 *gp = reinterpret_cast<int4 *>(gains + row * n_pad + col0);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int i = 4 * i4 + e;
-                        const int y2 = 2 * static_cast<int32_t>(v[i]);
-                        o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
-                    }
-                    __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));   // streaming: keep X/Q in L2
+            for (int i4 = 0; i4 < 8; ++i4) {
+                const int4 d = dg[i4];
+                int o[4];
+                const int dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int i = 4 * i4 + e;
+                    const int y2 = 2 * static_cast<int32_t>(v[i]);
+                    o[e] = dd[e] + (((bits >> i) & 1u) ? -y2 : y2);
                 }
+                __stcs(gp + i4, make_int4(o[0], o[1], o[2], o[3]));   // streaming: keep X/Q in L2
             }
         }
+    }
+}
+
+template <bool SYM>
+__device__ __forceinline__ int32_t epilogue_tile(uint32_t t_row, int64_t row, bool row_ok, int n0, int n_pad,
+                                                 int32_t *__restrict__ gains, int emit_gains, bool with_diag,
+                                                 const int32_t *sdiag, const uint64_t (&xw)[4]) {
+    using namespace dev;
+    int32_t partial = 0;
+    // double-buffered drain: chunk c + 1 is read from TMEM while chunk c is folded
+    // (tcgen05.wait::ld waits for every outstanding load, so the loads alternate buffers)
+    uint32_t va[32], vb[32];
+    tmem_ld_32x32b_x32(t_row, va);
+#pragma unroll 1
+    for (int c = 0; c < kBN / 32; c += 2) {
+        tmem_wait_ld();
+        tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>((c + 1) * 32), vb);
+        epilogue_chunk<SYM>(va, c, partial, row, row_ok, n0, n_pad, gains, emit_gains, with_diag, sdiag, xw);
+        tmem_wait_ld();
+        if (c + 2 < kBN / 32) tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>((c + 2) * 32), va);
+        epilogue_chunk<SYM>(vb, c + 1, partial, row, row_ok, n0, n_pad, gains, emit_gains, with_diag, sdiag, xw);
     }
     return partial;
 }
 
-// Work item -> (plane, M tile, N tile, K range).  f is linear in Y, so the partial row-dots
-// of K splits add up in the fold; the -Q_jj term of SYM goes with the split owning kb 0.
+// Work item -> (plane, M tile, split-table entry = (N tile, K block range)), plane outermost,
+// then M tile, then N tile.  f is linear in Y, so the partial row-dots of K splits add up in the
+// fold; the -Q_jj term of SYM goes with the split owning kb 0.
 struct Item {
-    int plane, mt, nt, ks, kb0, kb1;
+    int plane, mt, nt, sidx, kb0, kb1;
 };
 template <bool SYM>
 __device__ __forceinline__ Item decode_item(const EvalParams &p, int64_t item) {
     Item it;
-    const int64_t per_plane = p.mn_tiles * p.ksplit;
+    const int64_t per_plane = p.num_m_tiles * p.nsplit;
     it.plane = static_cast<int>(item / per_plane);
     const int64_t r = item - static_cast<int64_t>(it.plane) * per_plane;
-    const int64_t mn = r / p.ksplit;
-    it.ks = static_cast<int>(r - mn * p.ksplit);
-    it.mt = static_cast<int>(mn / p.num_n_tiles);
-    it.nt = static_cast<int>(mn - static_cast<int64_t>(it.mt) * p.num_n_tiles);
-    const int kbs = kbs_of(it.nt, p.num_k_blocks, SYM);
-    it.kb0 = it.ks * kbs / p.ksplit;
-    it.kb1 = (it.ks + 1) * kbs / p.ksplit;
+    it.mt = static_cast<int>(r / p.nsplit);
+    it.sidx = static_cast<int>(r - static_cast<int64_t>(it.mt) * p.nsplit);
+    const uint32_t e = p.split_tab[it.sidx];
+    it.nt = static_cast<int>(e & 0xFFu);
+    it.kb0 = static_cast<int>((e >> 8) & 0xFFu);
+    it.kb1 = static_cast<int>(e >> 16);
     return it;
 }
 __device__ __forceinline__ int64_t split_index(const EvalParams &p, const Item &it) {
-    return (static_cast<int64_t>(it.plane) * p.num_n_tiles + it.nt) * p.ksplit + it.ks;
+    return static_cast<int64_t>(it.plane) * p.nsplit + it.sidx;
 }
 
 // ---------------------------------------------------------------- single-CTA kernel (M = 128)
@@ -431,6 +481,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
     uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
     __shared__ __align__(16) int32_t s_diag[4 * kBN];   // per epilogue warp: the tile's diagonal slice
+    __shared__ int4 s_fold[kFoldBatch * 32];             // fold warp: one batch of staged partials
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -514,7 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
             const Item it = decode_item<SYM>(p, item);
             if (it.kb0 == it.kb1) continue;
             mbar_wait(&ffull[fslot], fphase);
-            fold_item<SYM>(p, it.mt, lane);
+            fold_item<SYM>(p, it.mt, lane, s_fold);
             __syncwarp();
             if (lane == 0) mbar_arrive(&fempty[fslot]);
             if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
@@ -532,12 +583,15 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
             if (it.kb0 == it.kb1) continue;
             const int64_t row = static_cast<int64_t>(it.mt) * kBM + row_in_tile;
             const bool row_ok = row < p.K;
+            uint64_t xw[4];
+            epilogue_stage<SYM>(row, row_ok, it.nt * kBN, p.W64, p.Xb, p.diag[it.plane], p.emit_gains, it.kb0 == 0,
+                                s_diag + quarter * kBN, lane, xw);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (warp == 2 && lane == 0) EV_STAMP(5);
             const int32_t partial = epilogue_tile<SYM>(
                 tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
-                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0,
-                s_diag + quarter * kBN, lane);
+                row_ok, it.nt * kBN, p.n_pad, p.gains, p.emit_gains, it.kb0 == 0, s_diag + quarter * kBN, xw);
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
@@ -579,6 +633,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     uint64_t *fempty = ffull + kFoldRing;     // fold warp -> epilogue (1 arrival)
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(fempty + kFoldRing);
     __shared__ __align__(16) int32_t s_diag[4 * kBN];   // per epilogue warp: the tile's diagonal slice
+    __shared__ int4 s_fold[kFoldBatch * 32];             // fold warp: one batch of staged partials
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -587,6 +642,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (threadIdx.x == 0) {
+        EV_STAMP(0);
         for (int s = 0; s < kPairStages; ++s) {
             mbar_init(&full[s], 1);           // the leader's expect_tx; both CTAs' bytes land here
             mbar_init(&empty[s], 1);          // multicast commit of the leader's MMAs
@@ -608,6 +664,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     cluster_sync();                           // barriers of both CTAs initialised, TMEM allocated
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) EV_STAMP(1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -629,6 +686,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
                     if (++stage == kPairStages) { stage = 0; phase ^= 1u; }
                 }
             }
+            EV_STAMP(2);
         }
     } else if (warp == 1) {
         if (lane == 0 && leader) {
@@ -646,6 +704,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
                 for (int kb = it.kb0; kb < it.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (kb == it.kb0 && item == cid) EV_STAMP(3);
                     const uint64_t adesc = umma_desc_sw128(smem_u32(sA + stage * kABytes));
                     const uint64_t bdesc = umma_desc_sw128(smem_u32(sB + stage * kABytes));
 #pragma unroll
@@ -658,6 +717,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
                 mma_commit_pair(&tfull[acc]);
                 if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
             }
+            EV_STAMP(4);
         }
     } else if (warp == 6) {
         // ---------------- fold warp (each CTA: its own group)
@@ -667,11 +727,13 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             const Item it = decode_item<SYM>(p, item);
             if (it.kb0 == it.kb1) continue;
             mbar_wait(&ffull[fslot], fphase);
-            fold_item<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane);
+            if (lane == 0) EV_STAMP(7);
+            fold_item<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane, s_fold);
             __syncwarp();
             if (lane == 0) mbar_arrive(&fempty[fslot]);
             if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
         }
+        if (lane == 0) EV_STAMP(8);
     } else {
         // ---------------- epilogue (both CTAs: their own 128 rows)
         const int quarter = warp & 3;
@@ -688,12 +750,15 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             const int64_t group = static_cast<int64_t>(it.mt) * 2 + rank;
             const int64_t row = group * kBM + row_in_tile;
             const bool row_ok = row < p.K;
+            uint64_t xw[4];
+            epilogue_stage<SYM>(row, row_ok, it.nt * kBN, p.W64, p.Xb, p.diag[it.plane], p.emit_gains, it.kb0 == 0,
+                                s_diag + quarter * kBN, lane, xw);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (warp == 2 && lane == 0) EV_STAMP(5);
             const int32_t partial = epilogue_tile<SYM>(
                 tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(acc * kBN), row,
-                row_ok, it.nt * kBN, p.W64, p.n_pad, p.Xb, p.diag[it.plane], p.gains, p.emit_gains, it.kb0 == 0,
-                s_diag + quarter * kBN, lane);
+                row_ok, it.nt * kBN, p.n_pad, p.gains, p.emit_gains, it.kb0 == 0, s_diag + quarter * kBN, xw);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
@@ -704,10 +769,12 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
             if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
         }
+        if (warp == 2 && lane == 0) EV_STAMP(6);
     }
 
     tc_fence_before();
     cluster_sync();                           // all MMAs retired, both epilogues done
+    if (threadIdx.x == 0) EV_STAMP(9);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_cg2(tmem_base, kTmemCols);
@@ -716,7 +783,22 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
 
 }  // namespace
 
-// Shapes of a launch (host): items, groups and the partial buffer it needs.
+#if UBQP_EVAL_TRACE
+// debug builds only: copy the per-CTA stamps of the last pair launch (512 x 16 ns timestamps)
+extern "C" int ubqp_debug_eval_trace(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, g_evtrace, sizeof(g_evtrace)) == cudaSuccess ? 0 : 1;
+}
+#endif
+
+// Shapes of a launch (host): items, groups, the K-split table and the partial buffer.
+// Items of one (M tile, plane) are the entries of the split table: N tile nt (its K blocks:
+// all of them, or, triangular, the kbs(nt) = min(num_k_blocks, 2 (nt + 1)) blocks of rows < 256
+// (nt + 1)) cut into s(nt) K ranges.  s(nt) = 1 unless an f-only CTA-pair launch has fewer
+// tiles than CTA pairs; then the K blocks are BALANCED over the pairs: the least T >= 2 with
+// num_m_tiles planes sum_nt ceil(kbs(nt) / T) <= pairs, s(nt) = ceil(kbs(nt) / T), so every
+// pair runs one item of <= T blocks (round 2's uniform power-of-two splits left the largest
+// tiles with 2x the blocks and some pairs with two items; measured at K = 1000: the MMA phase's
+// tail was 6.7 us against a 3.8 us median).  UBQP_KSPLIT = s forces s(nt) = min(s, kbs(nt)).
 EvalShape eval_shape(const Ctx &c, int64_t k, int planes, bool emit_gains, bool sym) {
     EvalShape s;
     s.pair = c.eval_pair;
@@ -725,34 +807,42 @@ EvalShape eval_shape(const Ctx &c, int64_t k, int planes, bool emit_gains, bool 
     const int rows = s.pair ? 2 * kBM : kBM;
     s.num_m_tiles = (k + rows - 1) / rows;
     s.mn_tiles = s.num_m_tiles * s.num_n_tiles;
-    s.ksplit = 1;
-    // f-only launches with fewer tiles than CTA pairs split K until every pair has one item
-    // (<= 8 ways): each extra item costs an epilogue and a fold, so splitting further loses
-    // (measured at K = 1000: n = 2500 15.9 us at 2 ways, 25.0 at 4, 48.8 at 8).  UBQP_KSPLIT
-    // forces a power of two (tuning sweeps).
     static const int forced = [] {
         const char *e = getenv("UBQP_KSPLIT");
         return e ? atoi(e) : 0;
     }();
-    if (s.pair && !emit_gains) {
-        if (forced > 0) {
-            while (s.ksplit < forced && s.ksplit < 16 && s.num_k_blocks >= 2 * s.ksplit) s.ksplit *= 2;
-        } else {
-            while (s.ksplit < 8 && s.mn_tiles * planes * s.ksplit < c.num_sms / 2 && s.num_k_blocks >= 4 * s.ksplit)
-                s.ksplit *= 2;
+    int kbs[64];
+    int total = 0;
+    for (int nt = 0; nt < s.num_n_tiles; ++nt) {
+        kbs[nt] = sym ? std::min(s.num_k_blocks, (nt + 1) * (kBN / kBK)) : s.num_k_blocks;
+        total += kbs[nt];
+    }
+    int T = 1 << 30;                                   // max K blocks per item (no split)
+    const int64_t pairs = c.num_sms / 2;
+    if (s.pair && !emit_gains && s.mn_tiles * planes < pairs) {
+        const int64_t per = pairs / (s.num_m_tiles * planes);   // items per (M tile, plane)
+        for (T = 2; T < s.num_k_blocks; ++T) {
+            int64_t cnt = 0;
+            for (int nt = 0; nt < s.num_n_tiles; ++nt) cnt += (kbs[nt] + T - 1) / T;
+            if (cnt <= per) break;
         }
     }
-    s.num_items = s.mn_tiles * planes * s.ksplit;
-    int nonempty = 0;
+    s.nsplit = 0;
     for (int nt = 0; nt < s.num_n_tiles; ++nt) {
-        const int kbs = sym ? std::min(s.num_k_blocks, (nt + 1) * (kBN / kBK)) : s.num_k_blocks;
-        for (int ks = 0; ks < s.ksplit; ++ks)
-            if ((ks + 1) * kbs / s.ksplit != ks * kbs / s.ksplit) ++nonempty;
+        int parts = (kbs[nt] + T - 1) / T;
+        if (s.pair && !emit_gains && forced > 0) parts = std::min(forced, kbs[nt]);
+        parts = std::max(1, std::min(parts, kMaxSplits - s.nsplit - (s.num_n_tiles - 1 - nt)));
+        for (int q = 0; q < parts; ++q) {
+            const int kb0 = q * kbs[nt] / parts, kb1 = (q + 1) * kbs[nt] / parts;
+            s.split_tab[s.nsplit++] = static_cast<uint32_t>(nt) | (static_cast<uint32_t>(kb0) << 8) |
+                                      (static_cast<uint32_t>(kb1) << 16);
+        }
     }
-    s.items_per_group = planes * nonempty;
+    s.num_items = s.num_m_tiles * planes * s.nsplit;
+    s.items_per_group = planes * s.nsplit;
     s.num_groups = s.num_m_tiles * (s.pair ? 2 : 1);
     s.part_ld = s.num_groups * kBM;
-    s.part_elems = static_cast<int64_t>(planes) * s.num_n_tiles * s.ksplit * s.part_ld;
+    s.part_elems = static_cast<int64_t>(planes) * s.nsplit * s.part_ld;
     return s;
 }
 
@@ -772,10 +862,10 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
     p.W64 = c.W64;
     p.num_n_tiles = s.num_n_tiles;
     p.num_k_blocks = s.num_k_blocks;
-    p.ksplit = s.ksplit;
-    p.ksplit_lg = __builtin_ctz(static_cast<unsigned>(s.ksplit));
+    p.nsplit = s.nsplit;
+    for (int o = 0; o < s.nsplit; ++o) p.split_tab[o] = s.split_tab[o];
     p.K = L.k;
-    p.mn_tiles = s.mn_tiles;
+    p.num_m_tiles = s.num_m_tiles;
     p.num_items = s.num_items;
     p.Xb = L.Xb;
     p.gains = L.emit_gains ? c.gains : nullptr;

@@ -128,9 +128,12 @@ __host__ __device__ __forceinline__ int64_t global_index(int64_t slot, int rank,
 }
 
 // Shape of one evaluation launch (eval_tc.cu)
+constexpr int kMaxSplits = 256;       // K-split table entries per (M tile, plane)
 struct EvalShape {
     bool pair;
-    int num_n_tiles, num_k_blocks, ksplit, items_per_group;
+    int num_n_tiles, num_k_blocks, items_per_group;
+    int nsplit;                         // items per (M tile, plane): (N tile, K range) table entries
+    uint32_t split_tab[kMaxSplits];     // nt | kb0 << 8 | kb1 << 16, N tile major
     int64_t num_m_tiles, mn_tiles, num_items, num_groups, part_ld, part_elems;
 };
 struct EvalLaunch {
