@@ -354,6 +354,13 @@ def run_ours(args, cfg, rank, world, local_rank):
                                        "bookkeeping (>= 0.5 instructions per variable) runs on its own pipe",
                     "kernel_cap": {"instructions_per_variable_on_busiest_pipe": kernel_ops,
                                    "peak": alu_peak / kernel_ops, "frac": upd * kernel_ops / alu_peak},
+                    # tools/pipebench.cu (profiles/r02_pipebench.log): a 1:1 IDP.2A + VIMNMX3 mix, the
+                    # warp kernel's per-variable pair, issues 2.563 warp instructions per SM cycle at 32
+                    # warps/SM -- 41 variable updates per SM cycle, the measured ceiling of that mix
+                    "measured_mix_ceiling": {"var_updates_per_sm_cycle": 2.563 / 2 * 32,
+                                             "peak": 148 * 2.563 / 2 * 32 * sm_mhz * 1e6,
+                                             "frac": upd / (148 * 2.563 / 2 * 32 * sm_mhz * 1e6),
+                                             "source": "tools/pipebench.cu, profiles/r02_pipebench.log"},
                     "algorithmic_work": "n variable updates (gain + running argmax) per flip step",
                     "why_not_hbm": "Q (49 MB int8) is L2-resident (ncu L2 hit 99.5%); the byte view is hbm_view",
                     "hbm_view": dict(roof_asc)}

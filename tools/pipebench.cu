@@ -1,0 +1,70 @@
+// pipebench.cu — issue rates of the ascent's inner-loop instructions on this GPU (warp
+// instructions per cycle per SM at 32 warps per SM), so the ascent roofline rests on measured
+// pipe rates.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/pipebench tools/pipebench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("%s\n", cudaGetErrorString(e_)); return 1; } } while (0)
+
+__device__ __forceinline__ int idp(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm volatile("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// KIND 0: 16 IDP.2A per iteration (16 independent chains)
+// KIND 2: the ascent's mix: 16 IDP.2A + 16 VIMNMX3 per iteration
+// KIND 3: 16 IMAD per iteration
+template <int KIND>
+__global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
+    int k[16], m[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) { k[i] = threadIdx.x * (i + 1); m[i] = threadIdx.x ^ i; }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            if (KIND == 0 || KIND == 2) k[i] = idp(a, b + i, k[i]);
+            if (KIND == 3) k[i] = k[i] * static_cast<int>(a) + static_cast<int>(b);
+            if (KIND == 2) m[i] = (i & 1) ? min(m[i], min(k[i], k[i ^ 1])) : max(m[i], max(k[i], k[i ^ 1]));
+        }
+    }
+    int s = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s ^= k[i] ^ m[i];
+    if (s == 0x12345) out[threadIdx.x] = s;
+}
+
+int main() {
+    int *out;
+    CK(cudaMalloc(&out, 4096));
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 8192, threads = 1024, blocks = sms;   // 32 warps per SM
+    const char *names[] = {"IDP.2A", "", "IDP.2A + VIMNMX3 (1:1)", "IMAD"};
+    const int ops[] = {16, 16, 32, 16};
+    for (int kind = 0; kind < 4; ++kind) {
+        if (kind == 1) continue;
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            if (kind == 0) bench<0><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 2) bench<2><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 3) bench<3><<<blocks, threads>>>(out, 3, 5, iters);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double warp_ops = static_cast<double>(blocks) * (threads / 32) * iters * ops[kind];
+        const double ghz = 1.965;                              // SM clock under load (bench clocks)
+        printf("%-24s %8.3f ms  %.3f warp-instr/cycle/SM  (%.2f lanes/cycle/SMSP) @%.3f GHz\n", names[kind], best,
+               warp_ops / (best * 1e-3 * ghz * 1e9) / sms, warp_ops * 32 / (best * 1e-3 * ghz * 1e9) / sms / 4, ghz);
+    }
+    return 0;
+}
