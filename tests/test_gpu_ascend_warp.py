@@ -142,3 +142,31 @@ def test_warp_ascent_invalid_slots_and_range():
         u.ascend(np.arange(2, dtype=np.int32), 2, 10)
     assert e.value.code == 3
     u.close()
+
+
+hyp = pytest.importorskip("hypothesis")
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=int(__import__("os").environ.get("UBQP_HYPO_EXAMPLES", 40)), deadline=None)
+@given(n=st.integers(1, 7168), density=st.sampled_from([0.02, 0.3, 1.0]), qmax=st.sampled_from([1, 3, 100, 127]),
+       seed=st.integers(0, 2**31 - 1), max_flips=st.sampled_from([0, 1, 17, 10**6]))
+def test_warp_ascent_random(n, density, qmax, seed, max_flips):
+    """Randomised: the warp kernel against O7 (oracle) on a few starts, and word for word
+    against the CTA kernel on the whole batch, over every chunk count NCH = 1..14."""
+    K = 12
+    Q = generate_Q(n, density, -qmax, qmax, seed=seed)
+    u = Ubqp(0)
+    u.load_Q(Q, K)
+    u.random(seed, K)
+    u.eval_batch(UBQP_EMIT_GAINS)
+    slots = np.arange(K, dtype=np.int32)
+    f, fl, b, key = _run(u, slots, max_flips, ASCENT_WARP)
+    f2, fl2, b2, key2 = _run(u, slots, max_flips, ASCENT_DENSE)
+    assert np.array_equal(f, f2) and np.array_equal(fl, fl2) and np.array_equal(b, b2) and key == key2
+    few = slots[:3] if n > 3000 else slots
+    X0 = oracle.random_solutions(n, seed, K)[few]
+    Xr, fr, flr = oracle.ascend(Q, X0, oracle.eval_batch(Q, X0, nthreads=8), max_flips, nthreads=8)
+    assert np.array_equal(f[few], fr) and np.array_equal(fl[few], flr)
+    assert np.array_equal(unpack_bits(b[few], n), Xr)
+    u.close()
