@@ -17,6 +17,10 @@ __device__ __forceinline__ int idp(uint32_t a, uint32_t b, int c) {
 // KIND 0: 16 IDP.2A per iteration (16 independent chains)
 // KIND 2: the ascent's mix: 16 IDP.2A + 16 VIMNMX3 per iteration
 // KIND 3: 16 IMAD per iteration
+// KIND 4: 16 IDP.2A + 16 two-input IMNMX;  KIND 5: 16 IDP.2A + 16 LOP3;  KIND 6: 16 IDP.2A with
+// the ascent's operand sharing (one multiplier register, one row word per 4) + 16 VIMNMX3 whose
+// two data operands are the IDP results just produced (max and min over the same pair);
+// KIND 7: 16 IDP.2A + 32 two-input IMNMX (the argmax without 3-input min/max)
 template <int KIND>
 __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
     int k[16], m[16];
@@ -28,6 +32,20 @@ __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
             if (KIND == 0 || KIND == 2) k[i] = idp(a, b + i, k[i]);
             if (KIND == 3) k[i] = k[i] * static_cast<int>(a) + static_cast<int>(b);
             if (KIND == 2) m[i] = (i & 1) ? min(m[i], min(k[i], k[i ^ 1])) : max(m[i], max(k[i], k[i ^ 1]));
+            if (KIND == 4) { k[i] = idp(a, b + i, k[i]); m[i] = max(m[i], k[i]); }
+            if (KIND == 5) { k[i] = idp(a, b + i, k[i]); m[i] = m[i] ^ (k[i] & 0x5555); }
+            if (KIND == 6) k[i] = idp((i & 1) ? a : b, b + (i >> 2), k[i]);
+            if (KIND == 7) { k[i] = idp(a, b + i, k[i]); m[i] = max(m[i], k[i]); m[i ^ 1] = min(m[i ^ 1], k[i]); }
+
+        }
+        if (KIND == 6) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                m[i] = max(m[i], max(k[i], k[i + 1]));
+                m[i + 1] = min(m[i + 1], min(k[i], k[i + 1]));
+                m[i + 2] = max(m[i + 2], max(k[i + 2], k[i + 3]));
+                m[i + 3] = min(m[i + 3], min(k[i + 2], k[i + 3]));
+            }
         }
     }
     int s = 0;
@@ -45,9 +63,10 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 8192, threads = 1024, blocks = sms;   // 32 warps per SM
-    const char *names[] = {"IDP.2A", "", "IDP.2A + VIMNMX3 (1:1)", "IMAD"};
-    const int ops[] = {16, 16, 32, 16};
-    for (int kind = 0; kind < 4; ++kind) {
+    const char *names[] = {"IDP.2A", "", "IDP.2A + VIMNMX3 (1:1)", "IMAD", "IDP.2A + IMNMX (1:1)",
+                           "IDP.2A + LOP3 (1:1)", "IDP.2A + VIMNMX3 (1:1/4)", "IDP.2A + 2 IMNMX (1:2)"};
+    const int ops[] = {16, 16, 32, 16, 32, 32, 32, 48};
+    for (int kind = 0; kind < 8; ++kind) {
         if (kind == 1) continue;
         float best = 1e30f;
         for (int rep = 0; rep < 3; ++rep) {
@@ -55,6 +74,11 @@ int main() {
             if (kind == 0) bench<0><<<blocks, threads>>>(out, 3, 5, iters);
             if (kind == 2) bench<2><<<blocks, threads>>>(out, 3, 5, iters);
             if (kind == 3) bench<3><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 4) bench<4><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 5) bench<5><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 6) bench<6><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 7) bench<7><<<blocks, threads>>>(out, 3, 5, iters);
+
             cudaEventRecord(e1);
             CK(cudaEventSynchronize(e1));
             float ms;
