@@ -14,6 +14,12 @@ __device__ __forceinline__ int idp(uint32_t a, uint32_t b, int c) {
     return d;
 }
 
+__device__ __forceinline__ int vmax(int a, int b) {
+    int d;
+    asm volatile("max.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
 // KIND 0: 16 IDP.2A per iteration (16 independent chains)
 // KIND 2: the ascent's mix: 16 IDP.2A + 16 VIMNMX3 per iteration
 // KIND 3: 16 IMAD per iteration
@@ -21,8 +27,45 @@ __device__ __forceinline__ int idp(uint32_t a, uint32_t b, int c) {
 // the ascent's operand sharing (one multiplier register, one row word per 4) + 16 VIMNMX3 whose
 // two data operands are the IDP results just produced (max and min over the same pair);
 // KIND 7: 16 IDP.2A + 32 two-input IMNMX (the argmax without 3-input min/max)
+__device__ __forceinline__ int idph(uint32_t a, uint32_t b, int c) {
+    int d;
+    asm volatile("dp2a.hi.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// KIND 9: the warp ascent's loop, per 32-bit row word: 4 IDP.2A (vector multipliers (C,0) and
+// (0,C), the word shared) into 4 keys, then a 3-input max and a 3-input min over each key pair
 template <int KIND>
 __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
+    if (KIND == 9) {
+        int K[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) K[i] = threadIdx.x * (i + 3);
+        uint32_t a0 = a * threadIdx.x & 0xFFFFu, a1 = (a * threadIdx.x) << 16;
+        uint32_t w = b ^ threadIdx.x;
+        int m0 = 0, m1 = 0, n0 = 0, n1 = 0;
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const uint32_t ww = w + q;
+                int &k0 = K[4 * q], &k1 = K[4 * q + 1], &k2 = K[4 * q + 2], &k3 = K[4 * q + 3];
+                k0 = idp(a0, ww, k0);
+                k1 = idp(a1, ww, k1);
+                k2 = idph(a0, ww, k2);
+                k3 = idph(a1, ww, k3);
+                m0 = max(m0, max(k0, k1));
+                n0 = min(n0, min(k0, k1));
+                m1 = max(m1, max(k2, k3));
+                n1 = min(n1, min(k2, k3));
+            }
+            w = w * 1664525u + static_cast<uint32_t>(m0 ^ n1);
+        }
+        int s = m0 ^ m1 ^ n0 ^ n1;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s ^= K[i];
+        if (s == 0x12345) out[threadIdx.x] = s;
+        return;
+    }
     int k[16], m[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) { k[i] = threadIdx.x * (i + 1); m[i] = threadIdx.x ^ i; }
@@ -35,6 +78,8 @@ __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
             if (KIND == 4) { k[i] = idp(a, b + i, k[i]); m[i] = max(m[i], k[i]); }
             if (KIND == 5) { k[i] = idp(a, b + i, k[i]); m[i] = m[i] ^ (k[i] & 0x5555); }
             if (KIND == 6) k[i] = idp((i & 1) ? a : b, b + (i >> 2), k[i]);
+            if (KIND == 1) m[i] = vmax(vmax(m[i], m[(i + 5) & 15]), m[(i + 9) & 15]);
+            if (KIND == 8) m[i] = vmax(m[i], m[(i + 5) & 15]);
             if (KIND == 7) { k[i] = idp(a, b + i, k[i]); m[i] = max(m[i], k[i]); m[i ^ 1] = min(m[i ^ 1], k[i]); }
 
         }
@@ -63,15 +108,18 @@ int main() {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 8192, threads = 1024, blocks = sms;   // 32 warps per SM
-    const char *names[] = {"IDP.2A", "", "IDP.2A + VIMNMX3 (1:1)", "IMAD", "IDP.2A + IMNMX (1:1)",
-                           "IDP.2A + LOP3 (1:1)", "IDP.2A + VIMNMX3 (1:1/4)", "IDP.2A + 2 IMNMX (1:2)"};
-    const int ops[] = {16, 16, 32, 16, 32, 32, 32, 48};
-    for (int kind = 0; kind < 8; ++kind) {
-        if (kind == 1) continue;
+    const char *names[] = {"IDP.2A", "VIMNMX3 alone", "IDP.2A + VIMNMX3 (1:1)", "IMAD", "IDP.2A + IMNMX (1:1)",
+                           "IDP.2A + LOP3 (1:1)", "IDP.2A + VIMNMX3 (1:1/4)", "IDP.2A + 2 IMNMX (1:2)", "IMNMX alone",
+                           "ascent loop (per word 4 IDP + 4 VIMNMX3)"};
+    const int ops[] = {16, 16, 32, 16, 32, 32, 32, 48, 16, 64};
+    for (int kind = 0; kind < 10; ++kind) {
         float best = 1e30f;
         for (int rep = 0; rep < 3; ++rep) {
             cudaEventRecord(e0);
             if (kind == 0) bench<0><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 1) bench<1><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 8) bench<8><<<blocks, threads>>>(out, 3, 5, iters);
+            if (kind == 9) bench<9><<<blocks, threads>>>(out, 3, 5, iters);
             if (kind == 2) bench<2><<<blocks, threads>>>(out, 3, 5, iters);
             if (kind == 3) bench<3><<<blocks, threads>>>(out, 3, 5, iters);
             if (kind == 4) bench<4><<<blocks, threads>>>(out, 3, 5, iters);
