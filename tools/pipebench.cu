@@ -37,16 +37,66 @@ __device__ __forceinline__ int idph(uint32_t a, uint32_t b, int c) {
 // (0,C), the word shared) into 4 keys, then a 3-input max and a 3-input min over each key pair
 template <int KIND>
 __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
-    if (KIND == 9) {
-        int K[32];
+    if (KIND == 11 || KIND == 12 || KIND == 13) {
+        // the replica with the row words read from shared memory, one LDS.128 per 4 words, like
+        // the kernel (KIND 12: each chunk's load address depends on the max chain two chunks back
+        // through a runtime zero, to force IDP.2A / VIMNMX3 interleaving)
+        __shared__ uint4 srow[14 * 32];
+        for (int i = threadIdx.x; i < 14 * 32; i += blockDim.x) srow[i] = make_uint4(a * i, b ^ i, a + i, b - i);
+        __syncthreads();
+        const int lane = threadIdx.x & 31;
+        int K[224];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) K[i] = threadIdx.x * (i + 3);
+        for (int i = 0; i < 224; ++i) K[i] = threadIdx.x * (i + 3);
+        uint32_t a0 = KIND == 13 ? a & 0xFFFFu : a * threadIdx.x & 0xFFFFu;   // 13: warp-uniform multipliers
+        uint32_t a1 = KIND == 13 ? a << 16 : (a * threadIdx.x) << 16;
+        int m0 = 0, m1 = 0, n0 = 0, n1 = 0;
+        const uint32_t zero = b >> 31;                    // 0 at run time, unknown to the compiler
+        for (int it = 0; it < iters; ++it) {
+            int hist[14];
+#pragma unroll
+            for (int c = 0; c < 14; ++c) {
+                uint32_t addr = static_cast<uint32_t>(__cvta_generic_to_shared(&srow[32 * c + lane]));
+                if (KIND == 12 && c >= 2)
+                    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(addr) : "r"(hist[c - 2]), "r"(zero), "r"(addr));
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+                const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int &k0 = K[16 * c + 4 * q], &k1 = K[16 * c + 4 * q + 1], &k2 = K[16 * c + 4 * q + 2],
+                        &k3 = K[16 * c + 4 * q + 3];
+                    k0 = idp(a0, wv[q], k0);
+                    k1 = idp(a1, wv[q], k1);
+                    k2 = idph(a0, wv[q], k2);
+                    k3 = idph(a1, wv[q], k3);
+                    m0 = max(m0, max(k0, k1));
+                    n0 = min(n0, min(k0, k1));
+                    m1 = max(m1, max(k2, k3));
+                    n1 = min(n1, min(k2, k3));
+                }
+                hist[c] = m0;
+            }
+            a0 ^= static_cast<uint32_t>(m0 & 1);
+        }
+        int s = m0 ^ m1 ^ n0 ^ n1;
+#pragma unroll
+        for (int i = 0; i < 224; ++i) s ^= K[i];
+        if (s == 0x12345) out[threadIdx.x] = s;
+        return;
+    }
+    if (KIND == 9 || KIND == 10) {
+        constexpr int NWD = KIND == 9 ? 8 : 56;           // row words per step (4 keys each)
+        int K[4 * NWD];
+#pragma unroll
+        for (int i = 0; i < 4 * NWD; ++i) K[i] = threadIdx.x * (i + 3);
         uint32_t a0 = a * threadIdx.x & 0xFFFFu, a1 = (a * threadIdx.x) << 16;
         uint32_t w = b ^ threadIdx.x;
         int m0 = 0, m1 = 0, n0 = 0, n1 = 0;
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < NWD; ++q) {
                 const uint32_t ww = w + q;
                 int &k0 = K[4 * q], &k1 = K[4 * q + 1], &k2 = K[4 * q + 2], &k3 = K[4 * q + 3];
                 k0 = idp(a0, ww, k0);
@@ -62,7 +112,7 @@ __global__ void bench(int *out, uint32_t a, uint32_t b, int iters) {
         }
         int s = m0 ^ m1 ^ n0 ^ n1;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s ^= K[i];
+        for (int i = 0; i < 4 * NWD; ++i) s ^= K[i];
         if (s == 0x12345) out[threadIdx.x] = s;
         return;
     }
@@ -137,6 +187,55 @@ int main() {
         const double ghz = 1.965;                              // SM clock under load (bench clocks)
         printf("%-24s %8.3f ms  %.3f warp-instr/cycle/SM  (%.2f lanes/cycle/SMSP) @%.3f GHz\n", names[kind], best,
                warp_ops / (best * 1e-3 * ghz * 1e9) / sms, warp_ops * 32 / (best * 1e-3 * ghz * 1e9) / sms / 4, ghz);
+    }
+    // the loop replica at the warp kernel's occupancy and beyond; 224 keys per lane like n = 7000
+    for (int wps : {8}) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            bench<10><<<sms, 32 * wps>>>(out, 3, 5, iters / 7);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double warp_ops = static_cast<double>(sms) * wps * (iters / 7) * 56 * 8;
+        printf("ascent loop replica, 224 keys, %2d warps/SM: %.3f warp-instr/cycle/SM = %.1f variable updates/SM cycle\n",
+               wps, warp_ops / (best * 1e-3 * 1.965e9) / sms, warp_ops / (best * 1e-3 * 1.965e9) / sms * 16);
+    }
+    for (int kind : {11, 12, 13}) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            if (kind == 11) bench<11><<<sms, 32 * 8>>>(out, 3, 5, iters / 7);
+            else if (kind == 12) bench<12><<<sms, 32 * 8>>>(out, 3, 5, iters / 7);
+            else bench<13><<<sms, 32 * 8>>>(out, 3, 5, iters / 7);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double warp_ops = static_cast<double>(sms) * 8 * (iters / 7) * 56 * 8;
+        printf("replica with LDS row words%s, 8 warps/SM: %.1f variable updates/SM cycle\n",
+               kind == 12 ? " + lag-2 address token" : (kind == 13 ? ", warp-uniform multipliers" : ""),
+               warp_ops / (best * 1e-3 * 1.965e9) / sms * 16);
+    }
+    for (int wps : {4, 8, 12, 16, 24}) {
+        float best = 1e30f;
+        for (int rep = 0; rep < 3; ++rep) {
+            cudaEventRecord(e0);
+            bench<9><<<sms, 32 * wps>>>(out, 3, 5, iters);
+            cudaEventRecord(e1);
+            CK(cudaEventSynchronize(e1));
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double warp_ops = static_cast<double>(sms) * wps * iters * 64;
+        printf("ascent loop replica, %2d warps/SM: %.3f warp-instr/cycle/SM = %.1f variable updates/SM cycle\n", wps,
+               warp_ops / (best * 1e-3 * 1.965e9) / sms, warp_ops / (best * 1e-3 * 1.965e9) / sms * 16);
     }
     return 0;
 }
