@@ -73,3 +73,37 @@ def test_fold_device_outputs_and_interleaved_handles():
     assert np.array_equal(f1.cpu().numpy(), fo1) and np.array_equal(f2.cpu().numpy(), fo2)
     assert s1.cpu().tolist()[:3] == oracle.stats(fo1).tolist()[:3]
     assert s2.cpu().tolist()[:3] == oracle.stats(fo2).tolist()[:3]
+
+
+@pytest.mark.parametrize("n,K", [(16000, 5), (9000, 300), (2500, 1000), (4097, 129)])
+@pytest.mark.parametrize("ksplit", ["0", "3", "16"])
+def test_fold_balanced_splits_large_n(n, K, ksplit, monkeypatch):
+    """f-only launches with fewer tiles than CTA pairs use the balanced K-split table
+    (eval_tc.cu eval_shape); at n = 16000 (63 N tiles) it has > 32 entries, so the fold stages
+    the partials in two batches.  UBQP_KSPLIT forces uniform splits of every tile (3: uneven
+    ranges, 16: clamped by the 256-entry table).  f and the statistics equal the oracle."""
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, oracle
+from inputs import generate_Q
+from paper_1706_00037_b200 import Ubqp, ubqp_stats
+Q = generate_Q({n}, 0.3, seed=7)
+u = Ubqp(0)
+u.load_Q(Q, {K})
+u.random(11, {K})
+X = oracle.random_solutions({n}, 11, {K})
+fo = oracle.eval_batch(Q, X, nthreads=8)
+so = oracle.stats(fo)
+for _ in range(2):
+    f = np.zeros({K}, np.int64)
+    st = ubqp_stats()
+    u.eval_batch(0, f, st)
+    assert np.array_equal(f, fo)
+    assert (st.sum, st.count, st.max_key) == (int(so[0]), {K}, int(so[2]))
+print("ok")
+"""
+    env = dict(os.environ, UBQP_KSPLIT=ksplit)       # read once per process: run in a child
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
