@@ -396,6 +396,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         if parity is not None:
             out["cpu_baseline"]["parity"] = parity
     if world == 1 and not args.no_projection:
+        ms._bench_ms_step = ms_step
         out["shard_projection"] = shard_projection(ms, x0_bits, f0, cfg, ms_step)
     if world == 1 and not args.no_table1:
         out["table1_eval_1000"] = table1_eval(local_rank)
@@ -429,7 +430,7 @@ def shard_projection(ms, x0_bits, f0, cfg, ms_step_1gpu):
     out = {"what": "per-rank shard rounds (O10 sharding, blocks of B consecutive g dealt round robin) timed one "
                    "after another on one B200; the projected G-GPU step is the slowest shard; collectives not "
                    "included", "ms_1gpu": ms_step_1gpu}
-    slots_per_wave = 148 * 6                                  # ascent CTAs resident at n = 7000
+    slots_per_wave = 148 * 8                                  # warp-ascent solutions resident at n = 7000
     for B, G in ((1, 2), (1, 8), (2, 2), (2, 4), (2, 8)):
         u.set_option(OPT_SHARD_BLOCK, B)
         per = []
@@ -454,7 +455,57 @@ def shard_projection(ms, x0_bits, f0, cfg, ms_step_1gpu):
                         "projected_evals_per_s": K / (mx * 1e-3),
                         "projected_speedup": ms_step_1gpu / mx}
     u.set_option(OPT_SHARD_BLOCK, 2)
+    try:
+        out["exchange_nccl_world1"] = nccl_exchange_cost(ms)
+    except Exception as e:                                    # keep the bench line on any failure
+        out["exchange_nccl_world1"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out
+
+
+def nccl_exchange_cost(ms, reps: int = 200):
+    """The per-round exchange of MultiStart (stats all-reduce SUM + MAX, best-key all-reduce MAX,
+    winner-bits broadcast) through NCCL on a world-size-1 process group on this GPU
+    (UBQP_FORCE_COLLECTIVES semantics): the launch/synchronisation cost of the collectives on the
+    library's stream.  A lower bound for G GPUs (no NVLink transfer at world size 1)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1706_00037_b200 import multistart as msmod
+    if dist.is_initialized():
+        return {"skipped": "a process group is already initialised"}
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29531")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+    force = msmod.FORCE_COLLECTIVES
+    msmod.FORCE_COLLECTIVES = True
+    try:
+        stats = ms.stats.clone()
+        key = torch.zeros(1, dtype=torch.int64, device=stats.device)
+        row = ms.bits[0].contiguous()
+        for _ in range(10):
+            msmod.combine_stats(stats)
+            msmod.combine_best(key, row)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            msmod.combine_stats(stats)
+            msmod.combine_best(key, row)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / reps * 1e3
+    finally:
+        msmod.FORCE_COLLECTIVES = force
+        dist.destroy_process_group()
+    return {"us_per_round": us, "backend": "nccl", "world": 1,
+            "what": "combine_stats + combine_best (3 all-reduces, 1 broadcast, their host reads) per round",
+            "fraction_of_step": us * 1e-3 / ms_step_hint(ms)}
+
+
+def ms_step_hint(ms):
+    return getattr(ms, "_bench_ms_step", 216.0)
 
 
 def cpu_baseline_split():

@@ -12,9 +12,11 @@ replicated; every other step runs in the kernels behind include/ubqp.h.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
+
 import torch
 import torch.distributed as dist
 
@@ -44,17 +46,26 @@ def paper_lambda(mean: float, start_value: int) -> float:
     return min(1.0, max(1e-6, start_value / mean))
 
 
+# UBQP_FORCE_COLLECTIVES=1 runs the exchange steps even at world size 1 (tests: the NCCL path
+# on a single GPU, tests/test_gpu_nccl.py); results are identical either way
+FORCE_COLLECTIVES = os.environ.get("UBQP_FORCE_COLLECTIVES", "0") == "1"
+
+
 def dist_info(group=None):
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(group), dist.get_world_size(group)
     return 0, 1
 
 
+def _collective(world: int) -> bool:
+    return world > 1 or (FORCE_COLLECTIVES and dist.is_available() and dist.is_initialized())
+
+
 # ---------------------------------------------------------------- exchange steps (tested on gloo)
 def combine_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
     """stats int64[4] = {sum, count, max_key, 0} per rank -> global (SUM, SUM, MAX) in place."""
     _, world = dist_info(group)
-    if world > 1:
+    if _collective(world):
         sc = stats[:2].clone()
         mk = stats[2:3].clone()
         dist.all_reduce(sc, op=dist.ReduceOp.SUM, group=group)
@@ -69,7 +80,7 @@ def combine_best(key: torch.Tensor, bits_row: torch.Tensor, group=None, block: i
     solution's bits on its rank).  Returns (global key, winner bits) on every rank: MAX of
     the keys, then a broadcast of the bits from the rank owning g = key_g (O10 sharding)."""
     rank, world = dist_info(group)
-    if world == 1:
+    if not _collective(world):
         return int(key.item()), bits_row
     gk = key.clone()
     dist.all_reduce(gk, op=dist.ReduceOp.MAX, group=group)
@@ -175,7 +186,7 @@ class MultiStart:
         m, T = u.screen(self.lam, mean_sum, mean_count, maxv, self.surv)
         u.ascend(self.surv, m, self.max_flips, self.f_asc, self.flips, self.bits, self.key)
         row = self.bits[0]
-        if m > 0 and self.world > 1:
+        if m > 0 and _collective(self.world):
             k_local = int(self.key.item())
             owner, slot = shard_owner(key_g(k_local), self.world, self.block) if k_local >= 0 else (-1, -1)
             if k_local >= 0 and owner == self.rank:
@@ -183,7 +194,7 @@ class MultiStart:
                                                                         device=self.surv.device)).item())
                 row = self.bits[i]
         best_key, best_bits = combine_best(self.key, row.contiguous(), self.group, self.block)
-        if self.world == 1 and m > 0:
+        if not _collective(self.world) and m > 0:
             best_key = int(self.key.item())
             slot = key_g(best_key)
             i = int(torch.searchsorted(self.surv[:m], torch.tensor([slot], dtype=torch.int32,
