@@ -477,7 +477,23 @@ def nccl_exchange_cost(ms, reps: int = 200):
         return {"skipped": "a process group is already initialised"}
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29531")
-    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+    # the bench prints ONE JSON line on stdout: keep NCCL's banner (written to fd 1) off it
+    saved_debug = os.environ.get("NCCL_DEBUG")
+    os.environ["NCCL_DEBUG"] = "WARN"
+    import sys
+    sys.stdout.flush()
+    fd1 = os.dup(1)
+    os.dup2(os.open(os.devnull, os.O_WRONLY), 1)
+    try:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
+        torch.distributed.barrier()
+    finally:
+        os.dup2(fd1, 1)
+        os.close(fd1)
+        if saved_debug is None:
+            os.environ.pop("NCCL_DEBUG", None)
+        else:
+            os.environ["NCCL_DEBUG"] = saved_debug
     force = msmod.FORCE_COLLECTIVES
     msmod.FORCE_COLLECTIVES = True
     try:
@@ -498,7 +514,14 @@ def nccl_exchange_cost(ms, reps: int = 200):
         us = e0.elapsed_time(e1) / reps * 1e3
     finally:
         msmod.FORCE_COLLECTIVES = force
-        dist.destroy_process_group()
+        sys.stdout.flush()
+        fd1 = os.dup(1)
+        os.dup2(os.open(os.devnull, os.O_WRONLY), 1)
+        try:
+            dist.destroy_process_group()
+        finally:
+            os.dup2(fd1, 1)
+            os.close(fd1)
     return {"us_per_round": us, "backend": "nccl", "world": 1,
             "what": "combine_stats + combine_best (3 all-reduces, 1 broadcast, their host reads) per round",
             "fraction_of_step": us * 1e-3 / ms_step_hint(ms)}
