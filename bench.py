@@ -468,6 +468,7 @@ def nccl_exchange_cost(ms, reps: int = 200):
     (UBQP_FORCE_COLLECTIVES semantics): the launch/synchronisation cost of the collectives on the
     library's stream.  A lower bound for G GPUs (no NVLink transfer at world size 1)."""
     import os
+    import sys
 
     import torch
     import torch.distributed as dist
@@ -480,16 +481,24 @@ def nccl_exchange_cost(ms, reps: int = 200):
     # the bench prints ONE JSON line on stdout: keep NCCL's banner (written to fd 1) off it
     saved_debug = os.environ.get("NCCL_DEBUG")
     os.environ["NCCL_DEBUG"] = "WARN"
-    import sys
-    sys.stdout.flush()
-    fd1 = os.dup(1)
-    os.dup2(os.open(os.devnull, os.O_WRONLY), 1)
-    try:
+
+    def quiet(fn):                                            # run fn with fd 1 on /dev/null
+        sys.stdout.flush()
+        fd1, null = os.dup(1), os.open(os.devnull, os.O_WRONLY)
+        os.dup2(null, 1)
+        try:
+            fn()
+        finally:
+            os.dup2(fd1, 1)
+            os.close(fd1)
+            os.close(null)
+
+    def init():
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", torch.cuda.current_device()))
-        torch.distributed.barrier()
+        dist.barrier()
+    try:
+        quiet(init)
     finally:
-        os.dup2(fd1, 1)
-        os.close(fd1)
         if saved_debug is None:
             os.environ.pop("NCCL_DEBUG", None)
         else:
@@ -514,14 +523,7 @@ def nccl_exchange_cost(ms, reps: int = 200):
         us = e0.elapsed_time(e1) / reps * 1e3
     finally:
         msmod.FORCE_COLLECTIVES = force
-        sys.stdout.flush()
-        fd1 = os.dup(1)
-        os.dup2(os.open(os.devnull, os.O_WRONLY), 1)
-        try:
-            dist.destroy_process_group()
-        finally:
-            os.dup2(fd1, 1)
-            os.close(fd1)
+        quiet(dist.destroy_process_group)
     return {"us_per_round": us, "backend": "nccl", "world": 1,
             "what": "combine_stats + combine_best (3 all-reduces, 1 broadcast, their host reads) per round",
             "fraction_of_step": us * 1e-3 / ms_step_hint(ms)}
