@@ -38,10 +38,9 @@ using namespace dev;
 
 constexpr int kOffW = 1 << 21;
 
-// volatile: NVVM keeps the updates in source order (word by word, each followed by its
-// max/min), which ptxas then interleaves across the FMA-heavy and ALU pipes; as plain asm NVVM
-// clustered every IDP.2A of the step ahead of the first VIMNMX3 (measured: the loop ran at 28.7
-// variable updates per SM cycle instead of 40+, tools/pipebench.cu replica)
+// volatile keeps the updates in source order in the PTX (word by word, each followed by its
+// max/min); the SASS order is ptxas's own (see the chain restart in the loop).  The measured
+// bench build uses the volatile form; UBQP_WARP_VOLATILE=0 is the plain-asm A/B variant.
 #ifndef UBQP_WARP_VOLATILE
 #define UBQP_WARP_VOLATILE 1
 #endif
@@ -74,8 +73,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 // K[li >> 4][li & 15] += v for a warp-UNIFORM local index li (v = 0 on every lane but the
 // owner of k*), keeping every key in its register across the dispatch.
-//   UBQP_WARP_DISPATCH 0: one switch over li whose leaves are single in-place adds;
-//   UBQP_WARP_DISPATCH 1 (default): a switch over the chunk, then 16 predicated adds.
+//   UBQP_WARP_DISPATCH 0 (default): one switch over li whose leaves are single in-place adds;
+//   UBQP_WARP_DISPATCH 1: a switch over the chunk, then 16 predicated adds (measured the same
+//   at n = 7000, slower at n <= 2500).
 #ifndef UBQP_WARP_DISPATCH
 #define UBQP_WARP_DISPATCH 0
 #endif
