@@ -116,6 +116,9 @@ __device__ __forceinline__ void add_key(int (&K)[NCH][16], int li, int v) {
 #endif
 }
 
+#ifndef UBQP_WARP_SHORT
+#define UBQP_WARP_SHORT 1
+#endif
 template <int NCH, int MINB>
 __global__ void __launch_bounds__(32, MINB)
 ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int q_ld, int W64,
@@ -177,6 +180,23 @@ ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         // (Delta + OFF) << 9 | (15 - c) << 5 | (31 - lane) (< 2^31) finds the largest Delta, then the
         // lowest j up to e; the winner lane's e and x come by one shuffle.
         const int best = max(mx, -mn);
+#if UBQP_WARP_SHORT
+        // (Delta + OFF) << 9 | (15 - c) << 5 == (key' >> 4) << 5, since the low byte of key' is
+        // 255 - li = (15 - c) << 4 | (15 - e): one shift and one OR before the REDUX; the chunk
+        // and lane parts of k* come from the REDUX value while the shuffle is in flight
+        const unsigned v = (static_cast<unsigned>(best) >> 4 << 5) | static_cast<unsigned>(31 - lane);
+        const unsigned wv = __reduce_max_sync(0xFFFFFFFFu, v);
+        const int wl = 31 - static_cast<int>(wv & 31u);
+        const int gv = static_cast<int>(wv >> 9) - kOffW;
+        const int kbase = 512 * (15 - static_cast<int>((wv >> 5) & 15u)) + 16 * wl;
+        const int info = __shfl_sync(0xFFFFFFFFu, (best & 255) | (best != mx ? 256 : 0), wl);
+        if (gv <= 0 || flips == max_flips) break;
+
+        // ---- stage row k* (= column k*, Q symmetric): each lane copies its own pieces
+        const int li = 255 - (info & 255);
+        const int xk = info >> 8;
+        const int kstar = kbase + 15 - (info & 15);
+#else
         const int lbest = 255 - (best & 255);      // this lane's li
         const unsigned v = (static_cast<unsigned>(best >> 8) << 9) |
                            (static_cast<unsigned>(15 - (lbest >> 4)) << 5) | static_cast<unsigned>(31 - lane);
@@ -190,6 +210,7 @@ ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         const int li = 255 - (info & 255);
         const int xk = info >> 8;
         const int kstar = (li >> 4) * 512 + 16 * wl + (li & 15);
+#endif
         // 32-bit row offset (kstar * q_ld < 7168 * 7168): a short dependent chain to the copies
         // (measured 1.113 -> 1.169 Gsteps/s at n = 7000 against the 64-bit product)
         const int8_t *src = qlane + static_cast<uint32_t>(kstar) * static_cast<uint32_t>(q_ld);
