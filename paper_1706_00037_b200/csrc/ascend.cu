@@ -247,6 +247,7 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
         // ---- flip k*
         const int kstar = static_cast<int>(gk >> 1);
         const int xk = static_cast<int>(gk & 1u);
+        UBQP_DCHECK(kstar >= 0 && kstar < n);
         const int C = xk ? -512 : 512;          // 512 d, d = 1 - 2 x_k*
         fv += gv;
         ++flips;

@@ -196,6 +196,7 @@ ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
         const int li = 255 - (info & 255);
         const int xk = info >> 8;
         const int kstar = kbase + 15 - (info & 15);
+        UBQP_DCHECK(kstar == (li >> 4) * 512 + 16 * wl + (li & 15));
 #else
         const int lbest = 255 - (best & 255);      // this lane's li
         const unsigned v = (static_cast<unsigned>(best >> 8) << 9) |
@@ -213,6 +214,7 @@ ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
 #endif
         // 32-bit row offset (kstar * q_ld < 7168 * 7168): a short dependent chain to the copies
         // (measured 1.113 -> 1.169 Gsteps/s at n = 7000 against the 64-bit product)
+        UBQP_DCHECK(kstar >= 0 && kstar < n && li < 16 * NCH && 512 * NCH <= q_ld);
         const int8_t *src = qlane + static_cast<uint32_t>(kstar) * static_cast<uint32_t>(q_ld);
 #pragma unroll
         for (int c = 0; c < NCH; ++c) cp_async16(sbuf + 512 * c, src + 512 * c);
@@ -229,6 +231,7 @@ ascend_warp_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int 
             add_key<NCH>(K, li, corr);
         }
         cp_async_wait();                           // this lane's own pieces only
+        UBQP_DCHECK(!owner || (li >> 4) < NCH);
         if (owner) asm volatile("st.shared.u8 [%0], %1;" ::"r"(sbuf + 512 * (li >> 4) + (li & 15)), "r"(0) : "memory");
 
         // ---- fused uniform update + next argmax (max chains and min chains over K)

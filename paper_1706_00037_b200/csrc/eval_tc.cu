@@ -200,6 +200,7 @@ __device__ __forceinline__ void fold_item(const EvalParams &p, int64_t group, in
     __int128 rsum = 0, rmax = 0;
     bool rhave = false;
     const int64_t row0 = group * 128 + 4 * lane;
+    UBQP_DCHECK(group < p.num_groups && row0 + 3 < p.part_ld);
     __int128 acc[4] = {0, 0, 0, 0};
     long long fs[4] = {0, 0, 0, 0};
     const int nsplit = p.nsplit;
@@ -458,6 +459,8 @@ __device__ __forceinline__ Item decode_item(const EvalParams &p, int64_t item) {
     it.nt = static_cast<int>(e & 0xFFu);
     it.kb0 = static_cast<int>((e >> 8) & 0xFFu);
     it.kb1 = static_cast<int>(e >> 16);
+    UBQP_DCHECK(it.nt < p.num_n_tiles && it.kb0 < it.kb1 && it.kb1 <= p.num_k_blocks && it.plane < p.planes &&
+                it.sidx < p.nsplit);
     return it;
 }
 __device__ __forceinline__ int64_t split_index(const EvalParams &p, const Item &it) {
@@ -595,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_tc_kernel(const __grid_const
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
             mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
+            UBQP_DCHECK(row < p.part_ld && split_index(p, it) < static_cast<int64_t>(p.planes) * p.nsplit);
             p.part[split_index(p, it) * p.part_ld + row] = partial;
             __syncwarp();
             if (lane == 0) mbar_arrive(&ffull[fslot]);        // release: the warp's partials are stored
@@ -763,6 +767,7 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
             mbar_wait(&fempty[fslot], fphase ^ 1u);           // the fold warp released this slot
+            UBQP_DCHECK(row < p.part_ld && split_index(p, it) < static_cast<int64_t>(p.planes) * p.nsplit);
             p.part[split_index(p, it) * p.part_ld + row] = partial;
             __syncwarp();
             if (lane == 0) mbar_arrive(&ffull[fslot]);        // release: the warp's partials are stored

@@ -193,6 +193,20 @@ int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *g
 
 // ------------------------------------------------------------------ device helpers
 #ifdef __CUDACC__
+// Device-side bounds checks for debug builds (UBQP_NVCC_EXTRA=-DUBQP_DEBUG_CHECKS=1): a failed
+// check traps the kernel (the call then returns UBQP_E_CUDA).  compute-sanitizer is closed on
+// the GPU pool, so the parity suites run against this build instead (tools/debug_checks.sh).
+#ifndef UBQP_DEBUG_CHECKS
+#define UBQP_DEBUG_CHECKS 0
+#endif
+#if UBQP_DEBUG_CHECKS
+#define UBQP_DCHECK(cond) \
+    do {                  \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define UBQP_DCHECK(cond) ((void)0)
+#endif
 namespace ubqp {
 namespace dev {
 
