@@ -259,7 +259,8 @@ ascend_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad
             }
         }
         constexpr int kfix = RELINK ? kOff : 0;   // k* leaves D
-        const uint4 *qrow = reinterpret_cast<const uint4 *>(qbase + static_cast<int64_t>(kstar) * q_ld);
+        // 32-bit row offset (kstar * q_ld < 2^31 for n <= 16384): a shorter chain to the row loads
+        const uint4 *qrow = reinterpret_cast<const uint4 *>(qbase + static_cast<uint32_t>(kstar) * static_cast<uint32_t>(q_ld));
         uint4 w[NCH];
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
