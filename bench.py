@@ -326,7 +326,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                  "frac_of_2x_bf16_sustained": eval_tops / int8_peak_sust,
                  "frac_of_spec_4500": eval_tops / 4500.0}
     from paper_1706_00037_b200.ubqp import Q_ASCENT_LAST
-    asc_kind = {1: "ascend_kernel", 2: "ascend_sparse_kernel", 3: "ascend_warp_kernel"}.get(
+    asc_kind = {1: "ascend_kernel", 2: "ascend_sparse_kernel", 3: "ascend_warp_kernel", 4: "ascend_mw_kernel"}.get(
         u.query(Q_ASCENT_LAST), "ascend_kernel")
     roof_asc = {"bound": "hbm", "achieved": asc_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": asc_gbs / peaks["hbm_gbs"], "traffic": traffic.get(asc_kind),

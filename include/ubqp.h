@@ -275,7 +275,7 @@ int ubqp_sync(ubqp_t h);
  * exponent w and limb count L (R22; integer Q: 0 and 1), the off-diagonal nonzeros of an
  * integer Q, 1 if its sparse rows (fixed-stride ELL rows, NEXT-3) were built (off-diagonal density <= 0.25),
  * the sharding block B, and the kernel of the last ubqp_ascend (0 none yet, 1 dense CTA, 2 sparse,
- * 3 dense warp per solution; see UBQP_OPT_ASCENT). */
+ * 3 dense warp per solution, 4 dense multi-warp; see UBQP_OPT_ASCENT). */
 enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KLOCAL = 4,
        UBQP_Q_LAUNCHES = 5, UBQP_Q_STREAM = 6, UBQP_Q_REAL_EXP = 7, UBQP_Q_IS_REAL = 8,
        UBQP_Q_EVAL_EXP = 9, UBQP_Q_EVAL_LIMBS = 10, UBQP_Q_NNZ = 11, UBQP_Q_SPARSE_ROWS = 12,
@@ -283,12 +283,14 @@ enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KL
 int ubqp_query(ubqp_t h, int what, int64_t *value);
 
 /* Kernel selection (results never depend on it; every choice is exact):
- *   UBQP_OPT_ASCENT     0 = automatic (a dense kernel at every density: the warp-per-solution
- *                       ascent for 4096 < n_pad <= 7168, the CTA ascent otherwise; the sparse-row kernel
- *                       measured slower at densities 0.02-0.2, DESIGN.md §7.4'), 1 = dense CTA
- *                       ascent (two or more warps per solution), 2 = sparse-row ascent (NEXT-3;
- *                       E_STATE if the sparse rows were not built), 3 = dense warp-per-solution
- *                       ascent (E_RANGE if n_pad > 7168).  Used by ubqp_ascend.
+ *   UBQP_OPT_ASCENT     0 = automatic (a dense kernel at every density: the CTA ascent for
+ *                       n_pad <= 4096, the warp-per-solution ascent for 4096 < n_pad <= 7168, the
+ *                       multi-warp ascent above; the sparse-row kernel measured slower at densities
+ *                       0.02-0.2, DESIGN.md §7.4'), 1 = dense CTA ascent (two or more warps per
+ *                       solution, byte masks), 2 = sparse-row ascent (NEXT-3; E_STATE if the sparse
+ *                       rows were not built), 3 = dense warp-per-solution ascent (E_RANGE if
+ *                       n_pad > 7168), 4 = dense multi-warp ascent (2-4 warps per solution, the
+ *                       keys of kernel 3; every n).  Used by ubqp_ascend.
  *   UBQP_OPT_EVAL_PAIR  1 = CTA-pair (cta_group::2) evaluation (default), 0 = single CTA.
  *   UBQP_OPT_EVAL_TRI   1 = f-only evaluations use the lower triangle of Q (default), 0 = full.
  *   UBQP_OPT_SHARD_BLOCK  B in [1, 4096], the sharding block (see Sharding; default 2); set it

@@ -17,8 +17,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libubqp.so"
 OBJ = PKG / "_obj"
-SOURCES = ["abi.cu", "gen.cu", "eval_tc.cu", "screen.cu", "ascend.cu", "ascend_real.cu", "ascend_sparse.cu", "ascend_warp.cu"]
-HEADERS = ["ubqp_internal.cuh"]
+SOURCES = ["abi.cu", "gen.cu", "eval_tc.cu", "screen.cu", "ascend.cu", "ascend_real.cu", "ascend_sparse.cu", "ascend_warp.cu", "ascend_mw.cu"]
+HEADERS = ["ubqp_internal.cuh", "warp_keys.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [

@@ -1087,7 +1087,7 @@ int ubqp_set_option(ubqp_t h, int what, int64_t value) {
     GUARD(h);
     switch (what) {
         case UBQP_OPT_ASCENT:
-            if (value < 0 || value > 3) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_ASCENT must be 0, 1, 2 or 3");
+            if (value < 0 || value > 4) return fail(h, UBQP_E_INVALID, "ubqp: UBQP_OPT_ASCENT must be in [0, 4]");
             h->asc_kernel = static_cast<int>(value);
             break;
         case UBQP_OPT_EVAL_PAIR:

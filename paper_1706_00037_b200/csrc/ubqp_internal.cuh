@@ -57,7 +57,7 @@ struct Ctx {
     int64_t nnz = 0;             // off-diagonal nonzeros
     int ell_stride = 0;
     uint32_t *ell = nullptr;     // [n][ell_stride]
-    int asc_kernel = 0;          // 0 auto, 1 dense CTA, 2 sparse, 3 dense warp (UBQP_OPT_ASCENT)
+    int asc_kernel = 0;          // 0 auto, 1 dense CTA, 2 sparse, 3 dense warp, 4 dense multi-warp (UBQP_OPT_ASCENT)
     int asc_last = 0;            // kernel of the last ascend (1 CTA, 2 sparse, 3 warp; UBQP_Q_ASCENT_LAST)
     uint64_t *seed = nullptr;    // [W64] staged diversification seed
     uint64_t *parents = nullptr; // [parents_cap][W64] staged blend parents (host callers)
@@ -184,6 +184,10 @@ bool ascent_uses_sparse(const Ctx &c);
 int ascend_warp_max_n();
 int launch_ascend_warp(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
                        int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
+// ascend_warp.cu: 2 or 3 warps per solution (n_pad <= ascend_mw_max_n()); 1 if out of range
+int ascend_mw_max_n();
+int launch_ascend_mw(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips, int64_t *f_dev,
+                     int32_t *flips_dev, uint64_t *bits_dev, int64_t *best_dev);
 // path relinking (O11) of batch slots toward guides[i mod n_guides] on the ascent kernel
 int launch_relink(Ctx &c, const int32_t *slots_dev, int64_t m, const uint64_t *guides_dev, int64_t n_guides,
                   int64_t *f_dev, int32_t *steps_dev, int32_t *sbest_dev, int32_t *len_dev, uint64_t *bits_dev,

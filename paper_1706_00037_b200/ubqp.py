@@ -50,7 +50,7 @@ def shard_owner(g: int, world: int, block: int = SHARD_BLOCK_DEFAULT):
     b, o = divmod(g, block)
     r, q = b % world, b // world
     return r, q * block + o
-ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE, ASCENT_WARP = 0, 1, 2, 3
+ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE, ASCENT_WARP, ASCENT_MW = 0, 1, 2, 3, 4
 
 
 class UbqpError(RuntimeError):

@@ -130,7 +130,7 @@ def test_warp_ascent_invalid_slots_and_range():
     assert f[0] == fr[0] and f[3] == fr[1] and fl[0] == flr[0] and fl[3] == flr[1]
     assert np.array_equal(unpack_bits(b[[0, 3]], n), Xr)
     u.close()
-    # n_pad > 7168: the warp kernel is out of range (E_RANGE); automatic selection uses the CTA kernel
+    # n_pad > 7168: the warp kernel is out of range (E_RANGE); automatic selection uses the multi-warp kernel
     n = 7169
     Q = generate_Q(n, 0.01, seed=1)
     u = Ubqp(0)
@@ -141,6 +141,9 @@ def test_warp_ascent_invalid_slots_and_range():
     with pytest.raises(UbqpError) as e:
         u.ascend(np.arange(2, dtype=np.int32), 2, 10)
     assert e.value.code == 3
+    u.set_option(OPT_ASCENT, ASCENT_AUTO)
+    u.ascend(np.arange(2, dtype=np.int32), 2, 10)
+    assert u.query(Q_ASCENT_LAST) == 4
     u.close()
 
 

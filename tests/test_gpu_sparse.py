@@ -90,7 +90,7 @@ def test_sparse_selection_and_errors():
         u.ascend(np.arange(K, dtype=np.int32), K, 100)
     assert e.value.code == 4
     with pytest.raises(UbqpError) as e:
-        u.set_option(OPT_ASCENT, 4)
+        u.set_option(OPT_ASCENT, 5)
     assert e.value.code == 1
     # automatic selection gives the same results either way
     sp = generate_Q(n, 0.1, seed=2)

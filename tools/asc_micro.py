@@ -1,6 +1,7 @@
 """SURVEY §8(d) ascent microbench A at n in {2500, 5000, 7000} (8192 random starts, full
-ascent): flip steps/s per n and per dense kernel (1 = CTA, 3 = warp per solution; UBQP_ASC_KERNELS
-="1,3"), on the library UBQP_LIB points at (A/B of kernel variants).
+ascent): flip steps/s per n and per dense kernel (1 = CTA, 3 = warp per solution, 4 = 2-3 warps per
+solution; UBQP_ASC_KERNELS="1,3"; UBQP_ASC_M starts), on the library UBQP_LIB points at (A/B of
+kernel variants).
     python tools/asc_micro.py [n ...]"""
 import os
 import sys
@@ -17,7 +18,7 @@ from paper_1706_00037_b200.ubqp import OPT_ASCENT  # noqa: E402
 
 def main():
     ns = [int(a) for a in sys.argv[1:]] or [2500, 5000, 7000]
-    m = 8192
+    m = int(os.environ.get("UBQP_ASC_M", 8192))
     st = torch.cuda.Stream()                 # a non-default stream shared with the library
     torch.cuda.set_stream(st)
     for n in ns:
