@@ -24,7 +24,7 @@
 //
 // Register budget: 16 NCH keys + ~30 per lane (no spills up to NCH = 14, n_pad <= 7168, at
 // 255 registers = 2 warps per SMSP).  Automatic selection uses it for n_pad > 4096, where it
-// measured faster than the CTA kernel; larger n use the CTA kernel.
+// measured faster than the CTA kernel; larger n use the multi-warp kernel (ascend_mw.cu, §7.4m).
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
