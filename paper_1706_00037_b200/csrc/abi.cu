@@ -76,6 +76,7 @@ void free_batch(Ctx &c) {
     dfree(c.Xb); dfree(c.X8); dfree(c.f); dfree(c.gains); dfree(c.surv); dfree(c.blk_count);
     dfree(c.asc_f); dfree(c.asc_flips); dfree(c.asc_bits); dfree(c.asc_slots); dfree(c.asc_aux);
     dfree(c.part); dfree(c.grp_cnt); dfree(c.grp_res); dfree(c.X8r);
+    dfree(c.part_poll); dfree(c.grp_poll);
     c.part_cap = c.grp_cap = 0;
     c.asc_cap = 0;
     c.k_max = 0; c.k_cap_pad = 0; c.k_local = -1;
@@ -152,25 +153,31 @@ int ensure_fold(ubqp_t h, const ubqp::EvalShape &s) {
     if (s.part_elems > h->part_cap) {
         CK(cudaStreamSynchronize(h->stream));
         dfree(h->part);
+        dfree(h->part_poll);
         h->part_cap = 0;
-        if (cudaMalloc(&h->part, s.part_elems * sizeof(int32_t)) != cudaSuccess) {
+        if (cudaMalloc(&h->part, s.part_elems * sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&h->part_poll, s.part_elems * sizeof(int32_t)) != cudaSuccess) {
             cudaGetLastError();
             return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the evaluation partials");
         }
+        CK(cudaMemsetAsync(h->part_poll, 0x80, s.part_elems * sizeof(int32_t), h->stream));
         h->part_cap = s.part_elems;
     }
     if (s.num_groups + 1 > h->grp_cap) {
         CK(cudaStreamSynchronize(h->stream));
         dfree(h->grp_cnt);
         dfree(h->grp_res);
+        dfree(h->grp_poll);
         h->grp_cap = 0;
         const int64_t cap = s.num_groups + 1;
         if (cudaMalloc(&h->grp_cnt, cap * sizeof(unsigned)) != cudaSuccess ||
-            cudaMalloc(&h->grp_res, cap * 4 * sizeof(int64_t)) != cudaSuccess) {
+            cudaMalloc(&h->grp_res, cap * 4 * sizeof(int64_t)) != cudaSuccess ||
+            cudaMalloc(&h->grp_poll, cap * 2 * sizeof(int64_t)) != cudaSuccess) {
             cudaGetLastError();
             return fail(h, UBQP_E_NOMEM, "ubqp: cannot allocate the evaluation counters");
         }
         CK(cudaMemsetAsync(h->grp_cnt, 0, cap * sizeof(unsigned), h->stream));
+        CK(cudaMemsetAsync(h->grp_poll, 0x80, cap * 2 * sizeof(int64_t), h->stream));
         h->grp_cap = cap;
     }
     return UBQP_OK;

@@ -70,6 +70,7 @@ struct EvalParams {
     int64_t num_groups;
     int64_t *grp_res;                     // [num_groups][4]
     int mode;                             // kFoldInt / kFoldPlane / kFoldReal
+    int poll;                             // 1: poll-mode fold (fold_item_poll; part / grp_res = the poll buffers)
     int64_t *f, *f2;                      // int f (kFoldInt, kFoldPlane); f2 optional second copy
     double *fr, *fr2;                     // real f (kFoldReal)
     int64_t *stats, *stats2;              // int: {sum, K, max_key, 0}; real: ubqp_stats_real words
@@ -170,6 +171,147 @@ __device__ __forceinline__ void warp_i128_reduce(__int128 &sm, __int128 &mx, boo
         const __int128 om = from_i128(mh, ml);
         if (oh && (!have || om > mx)) mx = om;
         have = have || oh;
+    }
+}
+
+// ---------------------------------------------------------------- poll-mode fold (small launches)
+// When every item of a launch is resident at once (items <= CTA pairs: the paper's Table 1
+// shape, K = 1000), the counter chain above is the launch's tail (the arrival
+// atomic with its release/acquire fences, then the partials' round trip, twice).  Here every
+// partial word is its own flag instead: the buffers hold the sentinel kPollSent32 (0x80808080;
+// |partial| <= 256 (2n 127 + 127) < 2^31 - 2^26 at n <= 16384, so it is never a partial) and
+// ONE fold warp per 128-row group -- the CTA that ran the group's split 0 -- polls the group's
+// partials with L2-only copies (cp.async.cg: every lane's pieces in flight at once) until no
+// word is the sentinel, folds f and {sum f, max_key} as above, and puts the sentinel back.
+// The group results are flagged the same way (0x8080808080808080: sum f and the key never take
+// it) and polled by group 0's folder, which writes the statistics.  No atomics, no fences:
+// each word is read only after its own value arrived.  Progress: a spinning fold warp blocks
+// no other warp (one item per CTA, so the epilogue never waits on the fold ring), and at most
+// one spinning CTA per group stays resident while the others finish their items and exit.
+constexpr int kPollSent32 = static_cast<int>(0x80808080u);
+constexpr long long kPollSent64 = static_cast<long long>(0x8080808080808080ull);
+#ifndef UBQP_POLL_LIMIT
+#define UBQP_POLL_LIMIT (1u << 26)   // polls before trapping (seconds): a broken launch fails loudly
+#endif
+
+__device__ __forceinline__ bool poll_has_sent(const int4 &t) {
+    return t.x == kPollSent32 || t.y == kPollSent32 || t.z == kPollSent32 || t.w == kPollSent32;
+}
+
+// stage nb 16-byte pieces (stride ld4 int4) from L2 into shared memory until none holds the
+// sentinel; returns with the pieces in sfold[32 u + lane]
+__device__ __forceinline__ void poll_pieces(const int4 *ptr0, int64_t ld4, int nb, int lane, int4 *sfold) {
+    const uint32_t sdst = dev::smem_u32(sfold) + 16u * lane;
+    unsigned want = nb >= 32 ? 0xFFFFFFFFu : ((1u << nb) - 1u);   // pieces still to (re)load
+    for (unsigned tries = 0;; ++tries) {
+        const int4 *ptr = ptr0;
+        for (int u = 0; u < nb; ++u, ptr += ld4)
+            if ((want >> u) & 1u)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 512u * u), "l"(ptr) : "memory");
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        unsigned again = 0;
+        for (int u = 0; u < nb; ++u)
+            if (((want >> u) & 1u) && poll_has_sent(sfold[32 * u + lane])) again |= 1u << u;
+        want = again;
+        if (__all_sync(0xFFFFFFFFu, want == 0u)) return;
+        if (tries > UBQP_POLL_LIMIT) __trap();
+    }
+}
+
+template <bool SYM>
+__device__ __forceinline__ void fold_item_poll(const EvalParams &p, int64_t group, int lane, int4 *sfold) {
+    const int64_t row0 = group * 128 + 4 * lane;
+    UBQP_DCHECK(p.mode == kFoldInt && p.planes == 1 && group < p.num_groups && row0 + 3 < p.part_ld);
+    const int nsplit = p.nsplit;
+    const int64_t ld4 = p.part_ld / 4;
+    long long sacc[4] = {0, 0, 0, 0};
+    int4 *base = reinterpret_cast<int4 *>(p.part + row0);
+    const int4 sent = make_int4(kPollSent32, kPollSent32, kPollSent32, kPollSent32);
+    for (int s0 = 0; s0 < nsplit; s0 += kFoldBatch) {
+        const int nb = min(kFoldBatch, nsplit - s0);
+        int4 *ptr = base + static_cast<int64_t>(s0) * ld4;
+        poll_pieces(ptr, ld4, nb, lane, sfold);
+        for (int u = 0; u < nb; ++u) {
+            const int4 t = sfold[32 * u + lane];
+            sacc[0] += t.x;
+            sacc[1] += t.y;
+            sacc[2] += t.z;
+            sacc[3] += t.w;
+            __stcg(ptr + static_cast<int64_t>(u) * ld4, sent);   // re-arm for the next launch
+        }
+    }
+    if (lane == 0) EV_STAMP(15);
+    long long isum = 0, ikey = -1;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t row = row0 + q;
+        if (row >= p.K) continue;
+        const long long fsum = sacc[q];
+        p.f[row] = fsum;
+        if (p.f2) p.f2[row] = fsum;
+        const unsigned r32 = static_cast<unsigned>(row), b32 = static_cast<unsigned>(p.shard_b);
+        const long long g = p.world == 1 ? static_cast<long long>(row)
+                                         : (static_cast<long long>(p.rank) + (r32 / b32) * static_cast<long long>(p.world)) * b32 + r32 % b32;
+        const long long key = static_cast<long long>((static_cast<unsigned long long>(fsum + (1ll << 40)) << 22) |
+                                                     static_cast<unsigned long long>((1ll << 22) - 1 - g));
+        isum += fsum;
+        ikey = max(ikey, key);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        isum += __shfl_xor_sync(0xffffffffu, isum, o);
+        ikey = max(ikey, __shfl_xor_sync(0xffffffffu, ikey, o));
+    }
+    if (lane == 0) {
+        EV_STAMP(11);
+        __stcg(reinterpret_cast<longlong2 *>(p.grp_res) + group, make_longlong2(isum, ikey));
+    }
+    if (group != 0) return;
+    // group 0's folder: every group's {sum f, max_key} -> the statistics
+    const int ng = static_cast<int>(p.num_groups);
+    long long S = 0, M = -1;
+    const longlong2 sent2 = make_longlong2(kPollSent64, kPollSent64);
+    for (int g0 = 0; g0 < ng; g0 += 32 * kFoldBatch) {
+        // piece u of lane = group g0 + 32 u + lane (16 bytes each); out-of-range lanes re-read group 0
+        const int nb = min(kFoldBatch, (ng - g0 + 31) / 32);
+        const uint32_t sdst = dev::smem_u32(sfold) + 16u * lane;
+        unsigned want = 0;
+        for (int u = 0; u < nb; ++u)
+            if (g0 + 32 * u + lane < ng) want |= 1u << u;
+        for (unsigned tries = 0;; ++tries) {
+            for (int u = 0; u < nb; ++u)
+                if ((want >> u) & 1u)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst + 512u * u),
+                                 "l"(reinterpret_cast<const longlong2 *>(p.grp_res) + g0 + 32 * u + lane) : "memory");
+            asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+            unsigned again = 0;
+            for (int u = 0; u < nb; ++u) {
+                const longlong2 v = reinterpret_cast<const longlong2 *>(sfold)[32 * u + lane];
+                if (((want >> u) & 1u) && (v.x == kPollSent64 || v.y == kPollSent64)) again |= 1u << u;
+            }
+            want = again;
+            if (__all_sync(0xFFFFFFFFu, want == 0u)) break;
+            if (tries > UBQP_POLL_LIMIT) __trap();
+        }
+        for (int u = 0; u < nb; ++u) {
+            const int g = g0 + 32 * u + lane;
+            if (g >= ng) continue;
+            const longlong2 v = reinterpret_cast<const longlong2 *>(sfold)[32 * u + lane];
+            S += v.x;
+            M = max(M, v.y);
+            __stcg(reinterpret_cast<longlong2 *>(p.grp_res) + g, sent2);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        M = max(M, __shfl_xor_sync(0xffffffffu, M, o));
+    }
+    if (lane == 0) {
+        EV_STAMP(13);
+        const long long out[4] = {S, static_cast<long long>(p.K), M, 0};
+        for (int i = 0; i < 4; ++i) {
+            p.stats[i] = out[i];
+            if (p.stats2) p.stats2[i] = out[i];
+        }
     }
 }
 
@@ -732,7 +874,11 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
             if (it.kb0 == it.kb1) continue;
             mbar_wait(&ffull[fslot], fphase);
             if (lane == 0) EV_STAMP(7);
-            fold_item<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane, s_fold);
+            if (p.poll) {
+                if (it.sidx == 0) fold_item_poll<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane, s_fold);
+            } else {
+                fold_item<SYM>(p, static_cast<int64_t>(it.mt) * 2 + rank, lane, s_fold);
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&fempty[fslot]);
             if (++fslot == kFoldRing) { fslot = 0; fphase ^= 1u; }
@@ -882,6 +1028,17 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
     p.num_groups = s.num_groups;
     p.grp_res = c.grp_res;
     p.mode = L.mode;
+    // poll-mode fold: CTA-pair launches of integer f whose items all run at once (one per pair)
+    static const bool poll_ok = [] {
+        const char *e = getenv("UBQP_EVAL_POLL");
+        return !(e && e[0] == '0');
+    }();
+    if (poll_ok && s.pair && L.mode == kFoldInt && L.op->planes == 1 && s.num_items <= c.num_sms / 2 &&
+        c.part_poll && c.grp_poll) {
+        p.poll = 1;
+        p.part = c.part_poll;
+        p.grp_res = c.grp_poll;
+    }
     p.f = L.f;
     p.f2 = L.f2;
     p.fr = L.fr;

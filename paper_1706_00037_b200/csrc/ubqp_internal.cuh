@@ -82,6 +82,10 @@ struct Ctx {
     unsigned *grp_cnt = nullptr; // [grp_cap] self-resetting arrival counters (last one: groups done)
     int64_t grp_cap = 0;
     int64_t *grp_res = nullptr;  // [grp_cap][4]
+    // poll-mode fold (small launches, eval_tc.cu): the same shapes, every word preset to the
+    // sentinel 0x80808080 (never a partial) / 0x8080808080808080 and reset by its reader
+    int32_t *part_poll = nullptr; // part_cap elements
+    int64_t *grp_poll = nullptr;  // [grp_cap][2]
     // ascent outputs scratch
     int64_t *asc_f = nullptr; int32_t *asc_flips = nullptr; uint64_t *asc_bits = nullptr;
     int32_t *asc_slots = nullptr; int32_t *asc_aux = nullptr; int64_t asc_cap = 0;
