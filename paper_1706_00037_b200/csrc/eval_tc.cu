@@ -808,6 +808,11 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     if (warp == 1) tmem_alloc_cg2(tmem_slot, kTmemCols);
     tc_fence_before();
     cluster_sync();                           // barriers of both CTAs initialised, TMEM allocated
+    // programmatic dependent launch (launch_eval): the next kernel on the stream may start its
+    // prologue now; this one waits here for its predecessor's completion (and memory) before it
+    // reads X or writes anything -- a no-op when launched without the attribute
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) EV_STAMP(1);
@@ -1058,10 +1063,27 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
             c.eval_pair_attr_set = true;
         }
         const int64_t pairs = s.num_items < c.num_sms / 2 ? s.num_items : c.num_sms / 2;
+        // programmatic stream serialization: the launch overlaps the predecessor's tail (its
+        // exiting CTAs free SMs for this one's prologue); the kernel's griddepcontrol.wait keeps
+        // every memory access after the predecessor completed.  UBQP_EVAL_PDL=0: plain launch.
+        static const bool pdl = [] {
+            const char *e = getenv("UBQP_EVAL_PDL");
+            return !(e && e[0] == '0');
+        }();
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute attr[1];
+        cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = kPairSmemBytes;
+        cfg.stream = c.stream;
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
         if (sym)
-            eval_tc_pair_kernel<true><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(p);
+            cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<true>, p);
         else
-            eval_tc_pair_kernel<false><<<static_cast<unsigned>(2 * pairs), kThreads, kPairSmemBytes, c.stream>>>(p);
+            cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<false>, p);
     } else {
         if (!c.eval_attr_set) {
             cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
