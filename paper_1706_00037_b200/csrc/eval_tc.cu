@@ -808,11 +808,14 @@ eval_tc_pair_kernel(const __grid_constant__ EvalParams p) {
     if (warp == 1) tmem_alloc_cg2(tmem_slot, kTmemCols);
     tc_fence_before();
     cluster_sync();                           // barriers of both CTAs initialised, TMEM allocated
-    // programmatic dependent launch (launch_eval): the next kernel on the stream may start its
-    // prologue now; this one waits here for its predecessor's completion (and memory) before it
-    // reads X or writes anything -- a no-op when launched without the attribute
+    // programmatic dependent launch (launch_eval): the next kernel on the stream may launch now.
+    // Only this kernel triggers early, so a predecessor still running is another evaluation,
+    // which writes f, the statistics, the gains and the fold buffers but never X8, the Q planes
+    // or the diagonals: the TMA producer and the MMA issuer (reads of X8 / Q, TMEM writes) start
+    // at once, the epilogue and fold warps wait for the predecessor's completion (and memory)
+    // before their first global access.  No-ops when launched without the attribute.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (warp >= 2) asm volatile("griddepcontrol.wait;" ::: "memory");
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) EV_STAMP(1);

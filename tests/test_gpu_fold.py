@@ -75,6 +75,42 @@ def test_fold_device_outputs_and_interleaved_handles():
     assert s2.cpu().tolist()[:3] == oracle.stats(fo2).tolist()[:3]
 
 
+@pytest.mark.parametrize("n,K,pair", [(2500, 1000, 1), (700, 3000, 1), (300, 200, 0)])
+def test_back_to_back_evals_overlap(n, K, pair):
+    """Chains of evaluations on one handle with device outputs and no host sync: the CTA-pair
+    kernel is launched with programmatic dependent launch (the next evaluation's TMA producer
+    and MMA issuer start while the previous one's fold still runs; poll-mode fold at n = 2500,
+    K = 1000, counters at K = 3000).  Every f and statistics buffer, the gains of the last
+    evaluation and an ascent reading them must equal the oracle."""
+    import oracle as O
+    from paper_1706_00037_b200.ubqp import ASCENT_AUTO, OPT_ASCENT  # noqa: F401
+    Q = generate_Q(n, 0.1 if n == 2500 else 0.7, seed=n + K)
+    u = Ubqp(0, stream=torch.cuda.current_stream().cuda_stream)
+    u.set_option(OPT_EVAL_PAIR, pair)
+    u.load_Q(Q, K)
+    u.random(77, K)
+    fs = [torch.full((K,), -1, dtype=torch.int64, device="cuda") for _ in range(9)]
+    ss = [torch.full((4,), -1, dtype=torch.int64, device="cuda") for _ in range(9)]
+    for i in range(9):
+        u.eval_batch(UBQP_EMIT_GAINS if i % 3 == 2 else 0, fs[i], ss[i])
+    slots = torch.arange(min(K, 64), dtype=torch.int32, device="cuda")
+    fa = torch.zeros(len(slots), dtype=torch.int64, device="cuda")
+    u.ascend(slots, len(slots), 10 * n, fa)
+    torch.cuda.synchronize()
+    X = O.random_solutions(n, 77, K)
+    fo = O.eval_batch(Q, X, nthreads=8)
+    st = O.stats(fo).tolist()[:3]
+    for i in range(9):
+        assert np.array_equal(fs[i].cpu().numpy(), fo), i
+        assert ss[i].cpu().tolist()[:3] == st, i
+    g = np.zeros((4, n), np.int32)
+    u.get_gains(0, 4, g)
+    assert np.array_equal(g, np.stack([O.gains(Q, X[i]) for i in range(4)]))
+    _, fr, _ = O.ascend(Q, X[:len(slots)], fo[:len(slots)], 10 * n, nthreads=8)
+    assert np.array_equal(fa.cpu().numpy(), fr)
+    u.close()
+
+
 @pytest.mark.parametrize("n,K", [(16000, 5), (9000, 300), (2500, 1000), (4097, 129)])
 @pytest.mark.parametrize("ksplit", ["0", "3", "16"])
 def test_fold_balanced_splits_large_n(n, K, ksplit, monkeypatch):
