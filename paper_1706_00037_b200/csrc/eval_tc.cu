@@ -50,14 +50,21 @@ constexpr size_t kPairSmemBytes = static_cast<size_t>(kPairStages) * kPairStageB
 constexpr uint32_t kIdescPair = dev::idesc_i8(2 * kBM, kBN);
 
 // Kernel arguments (one __grid_constant__ block: the B tensor maps of every plane included).
+// A/B only (launch-cost experiments): smaller parameter blocks for integer-only builds
+#ifndef UBQP_EVAL_PARAM_PLANES
+#define UBQP_EVAL_PARAM_PLANES kMaxPlanes
+#endif
+#ifndef UBQP_EVAL_PARAM_SPLITS
+#define UBQP_EVAL_PARAM_SPLITS kMaxSplits
+#endif
 struct EvalParams {
     CUtensorMap tmX;                      // A = X8
-    CUtensorMap tmB[kMaxPlanes];          // B per plane (256-row boxes single-CTA, 128-row pair)
-    const int32_t *diag[kMaxPlanes];      // per-plane diagonal (SYM term, gains)
+    CUtensorMap tmB[UBQP_EVAL_PARAM_PLANES];          // B per plane (256-row boxes single-CTA, 128-row pair)
+    const int32_t *diag[UBQP_EVAL_PARAM_PLANES];      // per-plane diagonal (SYM term, gains)
     int planes;
     int n_pad, W64, num_n_tiles, num_k_blocks;
     int nsplit;                           // items per (M tile, plane) = split_tab entries
-    uint32_t split_tab[kMaxSplits];       // entry o: N tile | kb0 << 8 | kb1 << 16 (host, eval_shape)
+    uint32_t split_tab[UBQP_EVAL_PARAM_SPLITS];       // entry o: N tile | kb0 << 8 | kb1 << 16 (host, eval_shape)
     int64_t K, num_m_tiles, num_items;
     const uint64_t *Xb;
     int32_t *gains;                       // EMIT_GAINS target [K][n_pad] (single plane launches)

@@ -48,6 +48,19 @@ def main():
     t1 = time.perf_counter()
     torch.cuda.synchronize()
     print(f"n={n} bare ctypes: host {(t1 - t0) / reps * 1e6:6.2f} us/call")
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        fn(h, 0, None, None)
+    t1 = time.perf_counter()
+    torch.cuda.synchronize()
+    print(f"n={n} bare ctypes, no outputs: host {(t1 - t0) / reps * 1e6:6.2f} us/call")
+    q = u.lib.ubqp_query
+    v = ctypes.c_int64()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        q(h, 0, ctypes.byref(v))
+    t1 = time.perf_counter()
+    print(f"n={n} ubqp_query (guard only): host {(t1 - t0) / reps * 1e6:6.2f} us/call")
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=torch.cuda.current_stream()):
         for _ in range(50):
