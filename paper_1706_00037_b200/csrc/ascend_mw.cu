@@ -19,15 +19,15 @@ using namespace dev;
 
 constexpr int kOffM = 1 << 22;   // |Delta| <= 254 n - 127 < 2^22 up to n = 16384
 
-// ---- NW warps per solution (n_pad > 7168, and A/B below it; NW in {2, 3, 4}).  Same keys and update as the
-// one-warp kernel, with the key offset 2^22 (|Delta| <= 254 n - 127 < 2^22 up to n = 16384, and
-// 256 (Delta + 2^22) + 255 < 2^31); warp w of the CTA owns j = 512 (NW c + w) + 16 L + e, so the row k* is staged
-// in shared memory in natural order and every lane still copies and reads only its own pieces.
-// The argmax is the warp REDUX + shuffle, then ONE cross-warp exchange: each warp's lane 0
-// publishes a 64-bit word (Delta + OFF, 15 - c, NW - 1 - w, 31 - L, key byte, x) into a
-// double-buffered slot (the slot of step t is rewritten at t + 2, after every warp passed the
-// barrier of t + 1), one bar.sync, and every warp takes the max of the NW words: the largest
-// Delta, then the lowest j = (c, w, L, e).
+// ---- NW warps per solution (n_pad > 7168, and A/B below it; NW in {2, 3, 4}).  Same keys and
+// update as the one-warp kernel, with the key offset 2^22 (|Delta| <= 254 n - 127 < 2^22 up to
+// n = 16384, and 256 (Delta + 2^22) + 255 < 2^31); warp w of the CTA owns
+// j = 512 (NW c + w) + 16 L + e, so the row k* is staged in shared memory in natural order and
+// every lane still copies and reads only its own pieces.  The argmax is the warp REDUX + shuffle,
+// then ONE cross-warp exchange: each warp's lane 0 publishes a 64-bit word (Delta + OFF, 15 - c,
+// NW - 1 - w, 31 - L, key byte, x) into a double-buffered slot (the slot of step t is rewritten
+// at t + 2, after every warp passed the barrier of t + 1), one bar.sync, and every warp takes the
+// max of the NW words: the largest Delta, then the lowest j = (c, w, L, e).
 template <int NCH, int NW, int MINB>
 __global__ void __launch_bounds__(32 * NW, MINB)
 ascend_mw_kernel(const int32_t *__restrict__ slots, int max_flips, int n, int n_pad, int q_ld, int W64,

@@ -50,6 +50,10 @@ def shard_owner(g: int, world: int, block: int = SHARD_BLOCK_DEFAULT):
     b, o = divmod(g, block)
     r, q = b % world, b // world
     return r, q * block + o
+
+
+# UBQP_OPT_ASCENT values (include/ubqp.h): automatic, dense CTA, sparse rows, one warp per
+# solution, 2-4 warps per solution
 ASCENT_AUTO, ASCENT_DENSE, ASCENT_SPARSE, ASCENT_WARP, ASCENT_MW = 0, 1, 2, 3, 4
 
 
