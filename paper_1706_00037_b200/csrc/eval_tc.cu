@@ -1090,10 +1090,15 @@ int launch_eval(Ctx &c, const EvalLaunch &L) {
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = pdl ? 1 : 0;
-        if (sym)
-            cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<true>, p);
-        else
-            cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<false>, p);
+        auto go = [&]() {
+            return sym ? cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<true>, p)
+                       : cudaLaunchKernelEx(&cfg, eval_tc_pair_kernel<false>, p);
+        };
+        if (go() != cudaSuccess && cfg.numAttrs) {   // a stream without programmatic launch: plain
+            cudaGetLastError();
+            cfg.numAttrs = 0;
+            go();                                    // errors reach the caller's CK_LAUNCH
+        }
     } else {
         if (!c.eval_attr_set) {
             cudaFuncSetAttribute(eval_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
