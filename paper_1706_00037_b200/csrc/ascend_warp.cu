@@ -236,8 +236,15 @@ void launch_w(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64_
               uint64_t *bits_dev, int64_t *best_dev) {
     // registers ~ 16 NCH keys + ~32; the register file is split per SMSP (16 K each), so the
     // resident warps per SM are 4 x floor(512 / registers): 8 at NCH = 14 (<= 255 registers)
-    constexpr int kRegs = ((16 * NCH + 32 + 7) / 8) * 8;
-    constexpr int kMinB = 4 * (512 / kRegs) > 32 ? 32 : 4 * (512 / kRegs);
+    // NCH = 9 fits 166 registers (3 warps per SMSP instead of 2): measured n = 4500 1.753 vs
+    // 1.563 Gsteps/s (profiles/r02_warp_slack.log); a 16-register slack elsewhere gained nothing
+    // (n = 2500: 2.79 vs 2.96 at 5 warps per SMSP) and spills at NCH = 3
+#ifndef UBQP_WARP_REGS_SLACK
+#define UBQP_WARP_REGS_SLACK 32   // A/B: the non-key registers budgeted per lane
+#endif
+    constexpr int kSlack = NCH == 9 ? 22 : UBQP_WARP_REGS_SLACK;
+    constexpr int kRegsB = ((16 * NCH + kSlack + 7) / 8) * 8;
+    constexpr int kMinB = 4 * (512 / kRegsB) > 32 ? 32 : 4 * (512 / kRegsB);
     static const size_t smem_extra = [] {     // occupancy experiments: pad the CTA's shared memory
         const char *e = getenv("UBQP_ASC_WARP_SMEM");
         return static_cast<size_t>(e ? atoi(e) : 0);
