@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 from inputs import generate_Q  # noqa: E402
 from paper_1706_00037_b200 import UBQP_EMIT_GAINS, Ubqp  # noqa: E402
-from paper_1706_00037_b200.ubqp import OPT_ASCENT  # noqa: E402
+from paper_1706_00037_b200.ubqp import OPT_ASCENT, Q_ASCENT_LAST  # noqa: E402
 
 
 def main():
@@ -32,7 +32,7 @@ def main():
         fo = torch.zeros(m, dtype=torch.int64, device="cuda")
         for kern in [int(k) for k in os.environ.get("UBQP_ASC_KERNELS", "1,3").split(",")]:
             if kern == 3 and n > 7168:
-                continue
+                continue            # kernel 0 (automatic) prints the kernel it chose
             u.set_option(OPT_ASCENT, kern)
             best = 1e9
             for _ in range(3):
@@ -43,7 +43,8 @@ def main():
                 torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1))
             steps = int(flips.sum().item())
-            print(f"n={n} kernel={kern}: {best:7.2f} ms  {steps / best / 1e6:6.3f} Gsteps/s  steps={steps} "
+            chose = f" (ran {u.query(Q_ASCENT_LAST)})" if kern == 0 else ""
+            print(f"n={n} kernel={kern}{chose}: {best:7.2f} ms  {steps / best / 1e6:6.3f} Gsteps/s  steps={steps} "
                   f"fsum={int(fo.sum().item())}", flush=True)
         u.close()
 
