@@ -283,9 +283,10 @@ enum { UBQP_Q_N = 0, UBQP_Q_NPAD = 1, UBQP_Q_W64 = 2, UBQP_Q_KMAX = 3, UBQP_Q_KL
 int ubqp_query(ubqp_t h, int what, int64_t *value);
 
 /* Kernel selection (results never depend on it; every choice is exact):
- *   UBQP_OPT_ASCENT     0 = automatic (a dense kernel at every density: the CTA ascent for
- *                       n_pad <= 4096, the warp-per-solution ascent for 4096 < n_pad <= 7168, the
- *                       multi-warp ascent above; the sparse-row kernel measured slower at densities
+ *   UBQP_OPT_ASCENT     0 = automatic (a dense kernel at every density, as measured fastest: the
+ *                       warp-per-solution ascent for 3584 < n_pad <= 7168 and for 1537-2048 and
+ *                       2561-3072, the CTA ascent for the other n_pad <= 3584, the multi-warp
+ *                       ascent above 7168; the sparse-row kernel measured slower at densities
  *                       0.02-0.2, DESIGN.md §7.4'), 1 = dense CTA ascent (two or more warps per
  *                       solution, byte masks), 2 = sparse-row ascent (NEXT-3; E_STATE if the sparse
  *                       rows were not built), 3 = dense warp-per-solution ascent (E_RANGE if

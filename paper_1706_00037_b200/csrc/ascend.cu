@@ -498,8 +498,13 @@ int launch_ascend(Ctx &c, const int32_t *slots_dev, int64_t m, int32_t max_flips
         c.asc_last = 2;
         return launch_ascend_sparse(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);
     }
-    // automatic: the warp-per-solution kernel where it measured faster (n_pad in (4096, 7168])
-    if (c.asc_kernel == 3 || (c.asc_kernel == 0 && c.n_pad > 4096 && c.n_pad <= ascend_warp_max_n())) {
+    // automatic: the warp-per-solution kernel where it measured faster than the CTA kernel
+    // (profiles/r02_small_n_kernels.log, 8192 starts): every n_pad in (3584, 7168] (4 KB rows:
+    // 1.95 vs 1.44 Gsteps/s at n = 4096) and the 4- and 6-chunk shapes (+3-4% at n = 2048,
+    // 3072); the CTA kernel keeps 1-3, 5 and 7 chunks (n = 500: 7.7 vs 6.9, n = 2560: 3.16 vs 2.96)
+    const int wch = (c.n_pad + 511) / 512;
+    const bool warp_auto = c.n_pad <= ascend_warp_max_n() && (wch >= 8 || wch == 4 || wch == 6);
+    if (c.asc_kernel == 3 || (c.asc_kernel == 0 && warp_auto)) {
         c.asc_last = 3;
         return launch_ascend_warp(c, slots_dev, m, max_flips, f_dev, flips_dev, bits_dev, best_dev);
     }

@@ -23,8 +23,9 @@
 // uniform update leaves the new key alone.  Padding variables (j >= n) hold K = 0.
 //
 // Register budget: 16 NCH keys + ~30 per lane (no spills up to NCH = 14, n_pad <= 7168, at
-// 255 registers = 2 warps per SMSP).  Automatic selection uses it for n_pad > 4096, where it
-// measured faster than the CTA kernel; larger n use the multi-warp kernel (ascend_mw.cu, §7.4m).
+// 255 registers = 2 warps per SMSP).  Automatic selection uses it for n_pad in (3584, 7168] and
+// the 4- and 6-chunk shapes, where it measured faster than the CTA kernel;
+// larger n use the multi-warp kernel (ascend_mw.cu, §7.4m).
 #include <climits>
 #include <cstdio>
 #include <cstdlib>

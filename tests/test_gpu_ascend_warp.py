@@ -59,8 +59,10 @@ def test_warp_ascent_matches_oracle(n):
     # the CTA kernel agrees word for word (padding bits included)
     f2, fl2, b2, key2 = _run(u, slots, 10 * n, ASCENT_DENSE)
     assert u.query(Q_ASCENT_LAST) == ASCENT_DENSE
-    _run(u, slots[:1], 1, ASCENT_AUTO)                # automatic: warp kernel for 4096 < n_pad <= 7168
-    assert u.query(Q_ASCENT_LAST) == (ASCENT_WARP if 4096 < -(-n // 128) * 128 <= 7168 else ASCENT_DENSE)
+    _run(u, slots[:1], 1, ASCENT_AUTO)                # automatic: include/ubqp.h UBQP_OPT_ASCENT
+    n_pad = -(-n // 128) * 128
+    nch = -(-n_pad // 512)
+    assert u.query(Q_ASCENT_LAST) == (ASCENT_WARP if n_pad <= 7168 and (nch >= 8 or nch in (4, 6)) else ASCENT_DENSE)
     assert np.array_equal(f, f2) and np.array_equal(fl, fl2) and np.array_equal(b, b2) and key == key2
     u.close()
 
