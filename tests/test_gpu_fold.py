@@ -111,6 +111,42 @@ def test_back_to_back_evals_overlap(n, K, pair):
     u.close()
 
 
+def test_evals_in_cuda_graph():
+    """Evaluations captured in a CUDA graph (the programmatic-launch edges between them become
+    graph edges) and replayed twice on new batches: f and the statistics equal the oracle.
+    (Replays bypass the handle's host-side state, so gains are not read back here.)"""
+    import oracle as O
+    n, K = 2500, 1000
+    Q = generate_Q(n, 0.1, seed=31)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    u = Ubqp(0, stream=s.cuda_stream)
+    u.load_Q(Q, K)
+    f = [torch.zeros(K, dtype=torch.int64, device="cuda") for _ in range(3)]
+    st = [torch.zeros(4, dtype=torch.int64, device="cuda") for _ in range(3)]
+    u.random(1, K)
+    for i in range(3):                          # warm-up: buffers sized outside the capture
+        u.eval_batch(UBQP_EMIT_GAINS if i == 1 else 0, f[i], st[i])
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(3):
+            u.eval_batch(UBQP_EMIT_GAINS if i == 1 else 0, f[i], st[i])
+    for seed in (5, 6):
+        u.random(seed, K)
+        for t in f + st:
+            t.fill_(-7)
+        g.replay()
+        torch.cuda.synchronize()
+        X = O.random_solutions(n, seed, K)
+        fo = O.eval_batch(Q, X, nthreads=8)
+        for i in range(3):
+            assert np.array_equal(f[i].cpu().numpy(), fo), (seed, i)
+            assert st[i].cpu().tolist()[:3] == O.stats(fo).tolist()[:3], (seed, i)
+    u.close()
+    torch.cuda.set_stream(torch.cuda.default_stream())
+
+
 @pytest.mark.parametrize("n,K", [(16000, 5), (9000, 300), (2500, 1000), (4097, 129)])
 @pytest.mark.parametrize("ksplit", ["0", "3", "16"])
 def test_fold_balanced_splits_large_n(n, K, ksplit, monkeypatch):
