@@ -214,7 +214,10 @@ void launch_mw(Ctx &c, const int32_t *slots, int64_t m, int32_t max_flips, int64
 #ifndef UBQP_MW_SLACK7
 #define UBQP_MW_SLACK7 36   // A/B: the non-key register budget at NCH = 7
 #endif
-    constexpr int kRegs = ((16 * NCH + (NCH == 9 ? 22 : (NCH == 7 ? UBQP_MW_SLACK7 : 36)) + 7) / 8) * 8;
+#ifndef UBQP_MW_SLACK5
+#define UBQP_MW_SLACK5 36   // A/B: the non-key register budget at NCH = 5
+#endif
+    constexpr int kRegs = ((16 * NCH + (NCH == 9 ? 22 : (NCH == 7 ? UBQP_MW_SLACK7 : (NCH == 5 ? UBQP_MW_SLACK5 : 36))) + 7) / 8) * 8;
     constexpr int kWarps = 4 * (512 / kRegs) > 32 ? 32 : 4 * (512 / kRegs);
     constexpr int kMinB = kWarps / NW < 1 ? 1 : kWarps / NW;
     const size_t smem = 512 * NW * NCH + 64;   // + 2 x 4 exchange words (16-byte aligned pairs)
